@@ -1,0 +1,248 @@
+"""Generate the golden fixtures in this directory from the REFERENCE package.
+
+Run here (not on the GPU box; /root/reference does not travel):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [case ...]
+
+Every array below is produced by the reference's own public functions
+(``heatwave.assemble_system``, ``SchurOperator.apply_array``,
+``PreconditionerKX.apply_array``, ``WaveletTransform.*``,
+``MultigridSolver.apply_rows``, ``pcg``).  The forcing part of f-hat follows
+``assemble_rhs`` (/root/reference/pkg/src/heatwave/system.py:295-324) with the
+load ``(N (x) M_x) F`` of the P1 x P1 interpolant of the nodal forcing F
+(SURVEY.md §8d); ``check_interpolant_load`` pins that identity against
+``assemble_load`` (spatial.py:269-300) with an interpolating callable.
+
+Inputs come from ``paper_2009_08875_b200.inputs`` (seeded, blockwise), so the
+GPU box regenerates them bit-for-bit and only outputs are stored.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import heatwave as hw  # noqa: E402  (the reference)
+from heatwave import system as hw_system  # noqa: E402
+from heatwave.solver import _dot, ParallelPlan  # noqa: E402
+
+from paper_2009_08875_b200 import inputs  # noqa: E402
+
+PROBE_SEED = 7
+
+
+def problem_for(d, dist):
+    u0 = inputs.u0_sines if dist == "uniform" else inputs.u0_modes()
+    return hw.ProblemData(D=np.eye(d), c=0.0, u0=u0)
+
+
+def stencil_table(asm):
+    """Per-level (A, M) stencil values read from the reference's CSR."""
+    out = []
+    for ops in hw.assemble_level_operators(asm.hierarchy):
+        A = ops.A_x.to_scipy().tocsr()
+        M = ops.M_x.to_scipy().tocsr()
+        n = A.shape[0]
+        r = n // 2
+        out.append(dict(n=n,
+                        A_off=(A[r].indices - r).tolist(), A=A[r].data.tolist(),
+                        M_off=(M[r].indices - r).tolist(), M=M[r].data.tolist()))
+    return out
+
+
+def forcing_part(asm, F):
+    """g-part of f-hat from nodal forcing F via the reference's functions."""
+    n_t, n_x = F.shape
+    y = np.empty((asm.test.N.rows, n_x))
+    tmp = np.empty_like(y)
+    hw_system._spatial(asm.spatial.M_x, F, tmp[:n_t], None)
+    hw_system._temporal(asm.test.N, tmp[:n_t], y, None)
+    ky = hw.apply_KY(asm.spatial, asm.test, asm.K_x, hw.SpaceTimeVector(y)).array
+    w1 = np.empty((n_t, n_x))
+    w2 = np.empty((n_t, n_x))
+    hw_system._temporal(asm.test.T.T, ky, w1, None)
+    hw_system._spatial(asm.spatial.M_x, w1, w2, None)
+    g_ss = w2.copy()
+    hw_system._temporal(asm.test.N.T, ky, w1, None)
+    hw_system._spatial(asm.spatial.A_x, w1, w2, None)
+    g_ss += w2
+    return y, ky, g_ss, asm.wavelet.transpose_apply_array(g_ss)
+
+
+LEAN_DROP = ("load", "ky", "g_ss", "g_hat", "u0_hat", "MxP", "AxP", "WP")
+
+
+def run_case(name, d, J, K, dist, full=True, workers=8, lean=False):
+    t0 = time.time()
+    problem = problem_for(d, dist)
+    asm = hw.assemble_system(problem, J, K, hw.SolveConfig())
+    n_t, n_x = asm.S.n_t, asm.S.n_x
+    F = inputs.forcing(dist, n_t, n_x)
+    y, ky, g_ss, g_hat = forcing_part(asm, F)
+    u0_hat = asm.rhs.u0_part.array
+    fhat = g_hat + u0_hat
+    u0proj = hw.project_initial(asm.hierarchy.finest, problem.u0)
+
+    plan = ParallelPlan.create(workers, n_t) if workers > 1 else None
+    pool = hw.WorkerPool(workers) if workers > 1 else None
+    z = asm.K_X.apply_array(fhat, pool)
+    rho0 = _dot(fhat, z, np.empty(n_t), pool)
+    eps = 1e-6 * np.sqrt(rho0)
+    res = hw.pcg(asm.S, asm.K_X, hw.SpaceTimeVector(fhat), eps, plan)
+    u = asm.wavelet.apply_array(res.w.array)
+    meta = dict(name=name, d=d, J=J, K=K, dist=dist, n_t=n_t, n_x=n_x,
+                seed_f=inputs.SEED_F, probe_seed=PROBE_SEED,
+                iterations=res.iterations, eps=eps, rho0=rho0,
+                kappa=res.kappa_estimate,
+                residual_norms=list(map(float, res.residual_norms)),
+                cg_alphas=list(map(float, res.cg_alphas)),
+                cg_betas=list(map(float, res.cg_betas)),
+                F_sum=float(F.sum()), fhat_norm=float(np.linalg.norm(fhat)),
+                u_norm=float(np.linalg.norm(u)),
+                w_norm=float(np.linalg.norm(res.w.array)),
+                stencils=stencil_table(asm))
+    arrays = dict(u0proj=u0proj)
+    rng = np.random.default_rng(PROBE_SEED)
+    idx = np.sort(rng.choice(n_t * n_x, size=min(4096, n_t * n_x), replace=False))
+    arrays["sample_idx"] = idx
+    arrays["u_sample"] = u.reshape(-1)[idx]
+    arrays["fhat_sample"] = fhat.reshape(-1)[idx]
+    if full:
+        P = np.random.default_rng(PROBE_SEED).standard_normal((n_t, n_x))
+        arrays.update(fhat=fhat, load=y, ky=ky, g_ss=g_ss, g_hat=g_hat,
+                      u0_hat=u0_hat, w=res.w.array, u=u)
+        arrays["WP"] = asm.wavelet.apply_array(P)
+        arrays["WtP"] = asm.wavelet.transpose_apply_array(P)
+        arrays["SP"] = asm.S.apply_array(P)
+        arrays["KXP"] = asm.K_X.apply_array(P)
+        mx = np.empty_like(P)
+        ax = np.empty_like(P)
+        hw_system._spatial(asm.spatial.M_x, P, mx, None)
+        hw_system._spatial(asm.spatial.A_x, P, ax, None)
+        arrays["MxP"], arrays["AxP"] = mx, ax
+        kx = np.empty_like(P)
+        asm.K_x.apply_rows(P, kx, 0, n_t)
+        arrays["KxP"] = kx
+        cj = np.empty_like(P)
+        lv = asm.wavelet.levels.level_of
+        for r in range(n_t):
+            cj[r] = asm.K_X.blocks[int(lv[r])].apply(P[r])
+        arrays["CjP"] = cj
+        if lean:
+            for key in LEAN_DROP:
+                arrays.pop(key)
+    if pool is not None:
+        pool.close()
+    meta["seconds"] = time.time() - t0
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+    with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(f"{name}: its={res.iterations} kappa={res.kappa_estimate} "
+          f"{meta['seconds']:.1f}s", flush=True)
+
+
+def mg_rows_case(name, d, K, rows=1):
+    """Full outputs of K_x (alpha=1, mu=0) and C_j (alpha=0.3, mu=2^j) MG
+    applies on seeded rows at a larger K (streaming-kernel sizes)."""
+    hier = hw.build_mesh_hierarchy(d, K)
+    ops = hw.assemble_level_operators(hier)
+    n = ops[-1].A_x.rows
+    B = np.random.default_rng(PROBE_SEED).standard_normal((rows, n))
+    arrays = dict()
+    meta = dict(name=name, d=d, K=K, n=n, rows=rows, probe_seed=PROBE_SEED,
+                solvers=[])
+    for (alpha, mu) in ((1.0, 0.0), (0.3, 2.0 ** 5), (0.3, 2.0 ** 10)):
+        mg = hw.make_solver(hier, alpha, mu, 2, 3, level_operators=ops)
+        X = np.empty_like(B)
+        mg.apply_rows(B, X, 0, rows)
+        key = f"a{alpha:g}_mu{mu:g}"
+        arrays[key] = X
+        meta["solvers"].append(dict(key=key, alpha=alpha, mu=mu))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+    with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(f"{name}: done", flush=True)
+
+
+def wavelet_case(name, J, cols):
+    lv = hw.build_wavelet(J)
+    wt = hw.WaveletTransform(lv)
+    P = np.random.default_rng(PROBE_SEED).standard_normal((2 ** J + 1, cols))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"),
+                        W=wt.apply_array(P), Wt=wt.transpose_apply_array(P))
+    with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+        json.dump(dict(name=name, J=J, cols=cols, probe_seed=PROBE_SEED), fh)
+    print(f"{name}: done", flush=True)
+
+
+def check_interpolant_load():
+    """(N (x) M_x) F == assemble_load of the P1 x P1 interpolant of F."""
+    for d, J, K in ((1, 3, 4), (2, 2, 3)):
+        hier = hw.build_mesh_hierarchy(d, K)
+        mesh = hier.finest
+        test = hw.assemble_temporal_test(J)
+        ops = hw.assemble_level_operators(hier)[-1]
+        n_t, n_x = 2 ** J + 1, ops.M_x.rows
+        F = np.random.default_rng(3).uniform(-1, 1, (n_t, n_x))
+        npts = 2 ** K
+
+        def g(t, pts):
+            # hat interpolation in time, P1 in space (quadrature points are
+            # element midpoints/Gauss points -> use barycentric evaluation)
+            k = min(int(t * 2 ** J), 2 ** J - 1)
+            s = t * 2 ** J - k
+            row = (1 - s) * F[k] + s * F[k + 1]
+            full = np.zeros(len(mesh.vertices))
+            full[mesh.interior] = row
+            from scipy.interpolate import LinearNDInterpolator, interp1d
+            if d == 1:
+                f = interp1d(mesh.vertices[:, 0], full)
+                return f(pts[:, 0])
+            # the mesh's triangles, not Delaunay's: evaluate per element
+            out = np.empty(len(pts))
+            gi = pts * npts
+            for q, p in enumerate(gi):
+                i0, j0 = np.floor(p).astype(int)
+                i0, j0 = min(i0, npts - 1), min(j0, npts - 1)
+                fx, fy = p[0] - i0, p[1] - j0
+                v = lambda a, b: full[(i0 + a) * (npts + 1) + (j0 + b)]
+                if fx >= fy:   # triangle (i,j),(i+1,j),(i+1,j+1)
+                    out[q] = v(0, 0) + fx * (v(1, 0) - v(0, 0)) + fy * (v(1, 1) - v(1, 0))
+                else:          # triangle (i,j),(i+1,j+1),(i,j+1)
+                    out[q] = v(0, 0) + fy * (v(0, 1) - v(0, 0)) + fx * (v(1, 1) - v(0, 1))
+            return out
+
+        load = hw.assemble_load(mesh, J, g).array
+        tmp = np.empty((n_t, n_x))
+        y = np.empty((test.N.rows, n_x))
+        hw_system._spatial(ops.M_x, F, tmp, None)
+        hw_system._temporal(test.N, tmp, y, None)
+        rel = np.abs(load - y).max() / np.abs(y).max()
+        print(f"interpolant load d={d}: rel diff {rel:.2e}")
+        assert rel < 1e-13
+
+
+CASES = {
+    "c1": lambda: run_case("c1", 2, 4, 4, "uniform"),
+    "d1": lambda: run_case("d1", 1, 6, 6, "normal"),
+    "c2s": lambda: run_case("c2s", 2, 3, 6, "uniform", lean=True),
+    "d2": lambda: run_case("d2", 1, 10, 10, "normal", full=False),
+    "cfg2": lambda: run_case("cfg2", 2, 8, 8, "uniform", full=False),
+    "mg8": lambda: mg_rows_case("mg8", 2, 8),
+    "mg1d10": lambda: mg_rows_case("mg1d10", 1, 10, rows=4),
+    "wav10": lambda: wavelet_case("wav10", 10, 3),
+    "load": check_interpolant_load,
+}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    for n in names:
+        CASES[n]()
