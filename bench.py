@@ -1,0 +1,368 @@
+"""Benchmark: space-time DoF x PCG iterations / s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one full PCG solve of S-hat w = f-hat to rtol 1e-6 (the BASELINE
+stopping rule sqrt(r^T K_X r) <= 1e-6 sqrt(f^T K_X f)) with f-hat resident
+in HBM.  value = N_dofs * iterations * steps / time (device time, CUDA events,
+max over ranks).  `e2e` repeats the measurement through the C ABI's host-
+buffer entry point hwg_solve_host: pinned host f-hat -> device, PCG, u = W w,
+device -> host, every step.  Inputs are seeded synthetic data of the
+BASELINE config's shape and distribution (no dataset exists).
+
+--impl reference times the reference's CPU algorithm -- the oracle port in
+oracle/ (C + OpenMP over all host cores; the reference itself is Python +
+numba and cannot travel to the GPU box) -- one PCG iteration per step.
+
+N > 1 (torchrun): every rank solves its own replica of the workload
+("weak" scaling, no collective on the data path; time-slab sharding across
+GPUs is not built yet).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2009_08875_b200 import inputs  # noqa: E402
+
+METRIC = "space-time DoFs x PCG iters/sec (rtol 1e-6)"
+UNIT = "DoF*it/s"
+
+
+def model_bytes_per_iteration(d, J, K, nu=3, cycles=2):
+    """SURVEY.md §8d streaming byte model for one PCG iteration (8 B/word)."""
+    n_t = 2 ** J + 1
+    sizes = [(2 ** l - 1) ** d for l in range(1, K + 1)]
+    n_x = sizes[-1]
+    N = n_t * n_x
+    wav = 2 * sum(2 ** j + 1 for j in range(1, J + 1)) * n_x
+    words = 2 * wav + 3 * N + 3 * N + 2 * N + 13 * N
+    mg = 0
+    for cyc in range(cycles):
+        for l in range(K, 1, -1):
+            n, nc = sizes[l - 1], sizes[l - 2]
+            zero = (l < K) or cyc == 0
+            mg += 3 * nu * n - (n if zero else 0) + 3 * n + (n + nc) + (2 * n + nc) + 3 * nu * n
+        mg += 2 * sizes[0]
+    words += 4 * n_t * mg
+    return 8.0 * words
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg):
+    d, J, K, dist, u0 = inputs.recipe(cfg)
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** d
+    return d, J, K, dist, u0, n_t, n_x
+
+
+# --------------------------------------------------------------------------
+# CPU oracle legs (cpu_baseline and --impl reference)
+# --------------------------------------------------------------------------
+def oracle_setup(cfg, fhat=None, max_dofs=4.5e7):
+    """Oracle system for the workload (or a reduced-N_t twin with the same
+    N_x when the full config does not fit host RAM), its f-hat, and a label."""
+    from oracle import heatwave_oracle as O
+    d, J, K, dist, u0, n_t, n_x = workload(cfg)
+    Jo = J
+    while (2 ** Jo + 1) * n_x > max_dofs and Jo > 2:
+        Jo -= 1
+    system = O.assemble(d, Jo, K)
+    nto = 2 ** Jo + 1
+    if fhat is not None and Jo == J:
+        f = np.ascontiguousarray(fhat)
+    else:
+        f = system.rhs(inputs.forcing(dist, nto, n_x), u0)
+    label = (f"cfg{cfg} full size" if Jo == J else
+             f"reduced-N_t twin of cfg{cfg}: J={Jo} (N_t={nto}), same N_x={n_x}")
+    return O, system, f, label
+
+
+def oracle_iterations(O, system, f, iters):
+    """Time `iters` PCG iterations of the oracle (solver.py:212-256 body),
+    after an untimed setup (r = f, z = K r, p = z)."""
+    r = f.copy()
+    z = system.kx(r)
+    rho = O.dot(r, z)
+    p = z.copy()
+    w = np.zeros_like(f)
+    q = np.empty_like(f)
+    times = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        q[...] = system.schur(p)
+        alpha = rho / O.dot(p, q)
+        O.axpy(alpha, p, w)
+        O.axpy(-alpha, q, r)
+        system.kx(r, z)
+        rho_new = O.dot(r, z)
+        beta, rho = rho_new / rho, rho_new
+        O.xpay(beta, z, p)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import heatwave_oracle as O
+    threads = O.lib().or_num_threads()
+    O_, system, f, label = oracle_setup(args.config)
+    n = f.size
+    oracle_iterations(O_, system, f, args.warmup)
+    times = oracle_iterations(O_, system, f, args.steps)
+    t = sum(times)
+    value = n * args.steps / t
+    d, J, K, *_ = workload(args.config)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE recipe)",
+        "config": {"workload": f"cfg{args.config}", "sample": label, "d": d, "J": J, "K": K},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} PCG iterations, {label}, oracle/ C+OpenMP"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# GPU leg
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import paper_2009_08875_b200 as hw
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    d, J, K, dist_name, u0, n_t, n_x = workload(args.config)
+    N = n_t * n_x
+    problem = hw.ProblemData(D=np.eye(d), c=0.0, u0=u0)
+    F = inputs.forcing(dist_name, n_t, n_x)
+    asm = hw.assemble_system(problem, J, K, hw.SolveConfig(device=local), forcing=F,
+                             host_rhs=False)
+    del F
+    ctx = asm.ctx
+    f = asm.rhs.f_hat.array
+    w = torch.empty_like(f)
+    st = torch.cuda.current_stream(dev)
+
+    def solve():
+        stats, rc = ctx.pcg(f, w, 0.0, 1e-6, 200, 50)
+        if rc != 0:
+            raise RuntimeError(f"PCG failed with code {rc}")
+        return stats
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    its = None
+    for _ in range(args.warmup):
+        its = solve()["iterations"]
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = ctx.launches
+    ctx.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(st)
+        its_list = [solve()["iterations"] for _ in range(args.steps)]
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    launches = ctx.launches - launches0
+    barrier()
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    total_its = sum(its_list)
+    value = N * total_its * world / (ms_max / 1e3)
+
+    # roofline of the dominant kernel class
+    peak, peak_src = measured_peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dbytes, dn) = dom
+    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(dname)
+    model = model_bytes_per_iteration(d, J, K)
+    it_s = (ms_max / 1e3) / total_its
+
+    # end-to-end through the C ABI with host buffers
+    fh = torch.empty((n_t, n_x), dtype=torch.float64, pin_memory=True)
+    fh.copy_(f)
+    uh = torch.empty((n_t, n_x), dtype=torch.float64, pin_memory=True)
+    fh_np, uh_np = fh.numpy(), uh.numpy()
+    ctx.solve_host(fh_np, uh_np, 0.0, 1e-6)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_its = 0
+    for _ in range(args.steps):
+        s, rc = ctx.solve_host(fh_np, uh_np, 0.0, 1e-6)
+        if rc != 0:
+            raise RuntimeError(f"solve_host failed with code {rc}")
+        e2e_its += s["iterations"]
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = N * e2e_its * world / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import heatwave_oracle as O
+        O_, system, fo, label = oracle_setup(args.config, fhat=f.cpu().numpy())
+        n_iter = args.cpu_iterations
+        times = oracle_iterations(O_, system, fo, n_iter)
+        cpu = {"value": fo.size * n_iter / sum(times), "unit": UNIT,
+               "cores": O.lib().or_num_threads(), "kind": "port",
+               "sample": f"{n_iter} PCG iterations of the oracle (oracle/ C+OpenMP), {label}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE recipe: F~U[-1,1] nodal forcing, u0=sin sin)",
+            "config": {"workload": f"cfg{args.config}: {d}D heat, J={J} (N_t={n_t}), "
+                                   f"K={K} (N_x={n_x}), PCG to rtol 1e-6",
+                       "dofs": N, "iterations_per_solve": its_list[0],
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (each solve streams >100 arrays of "
+                             f"{8 * N / 1e6:.0f} MB)"},
+            "time_to_solve_s": ms_max / 1e3 / args.steps,
+            "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "launches": dn, "bytes_per_launch": dbytes / max(dn, 1),
+                         "peak_source": peak_src},
+            "roofline_model": {"bytes_per_iteration": model, "s_per_iteration": it_s,
+                               "achieved_GBs": model / it_s / 1e9,
+                               "frac": model / it_s / 1e9 / peak,
+                               "source": "SURVEY.md §8d streaming model"},
+            "kernel_classes_ms": {k: v[0] for k, v in prof.items()},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                    "d2h_bytes_per_step": 8 * N, "time_to_solve_s": e2e_s / args.steps},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=(1, 2, 3, 4))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cpu-iterations", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,186 @@
+/*
+ * heatwave_b200.h -- C ABI of the B200 space-time PCG hot path.
+ *
+ * Drop-in boundary for the reference package `heatwave`
+ * (/root/reference/pkg/src/heatwave).  The reference has no formal plugin
+ * API: its hot path sits behind a duck-typed operator protocol consumed by
+ * `pcg` and behind numba kernels on flat numpy arrays.  Each
+ * entry point below replaces one of those call sites; the Python mirror in
+ * paper_2009_08875_b200/ binds them with ctypes and maps return codes to the
+ * reference's exceptions.
+ *
+ * Conventions
+ *  - Space-time arrays are fp64, C-contiguous (rows, N_x): row j holds the
+ *    spatial coefficients of temporal DOF j (sparse.py:132-175).
+ *  - Every array pointer is a DEVICE pointer unless the name says `host`.
+ *    The caller owns inputs and outputs; the context owns its workspaces
+ *    (system.py:93-101: one solve per operator instance at a time).
+ *  - `stream` is a cudaStream_t passed as void*; NULL = legacy default.
+ *    All work is stream-ordered; calls return once the work is enqueued,
+ *    except hwg_pcg (which reads two scalars back per iteration) and
+ *    hwg_dot (which returns a host scalar).
+ *  - Return codes: HWG_OK or one of the HWG_E* codes; hwg_last_error()
+ *    gives a message for the calling thread.
+ */
+#ifndef HEATWAVE_B200_H
+#define HEATWAVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    HWG_OK = 0,
+    HWG_EINVAL = 1,     /* ValueError   (solver.py:185, system.py:190, wavelet.py:140, multigrid.py:49) */
+    HWG_ENOTSPD = 2,    /* RuntimeError p^T S p <= 0 (solver.py:217-219) */
+    HWG_EMAXIT = 3,     /* IterationLimitError (solver.py:132-137, 258-260) */
+    HWG_ECUDA = 4,      /* CUDA runtime failure */
+    HWG_ENOMEM = 5,     /* device allocation failed (cli.py:236-241 maps MemoryError) */
+    HWG_EKEY = 6        /* KeyError: no preconditioner block for a level (system.py:253-255) */
+};
+
+/* Number of stencil slots per (operator, level) in the coefficient table. */
+#define HWG_COEF_STRIDE 8
+
+/*
+ * Problem description.  Mirrors what assemble_system (solver.py:353-386)
+ * builds: temporal trial/test matrices (temporal.py:82-144), per-level P1
+ * stencils (spatial.py:202-229), the K_x solver (alpha=1, mu=0) and the
+ * J+1 blocks C_j (alpha, mu=2^j) of K_X (solver.py:372-377).
+ *
+ * coef: table [(J + 2) operators][K + 1 levels][HWG_COEF_STRIDE] doubles
+ *   (host memory, copied at create).  Operator 0 is K_x, operator 1 + j is
+ *   C_j.  Level l in 1..K (slot 0 unused).  Slots:
+ *     2D: 0 centre, 1 x-neighbours (i+-1), 2 y-neighbours (j+-1),
+ *         3 diagonal (i+1,j+1)/(i-1,j-1), 4 1/centre, 5 coarse inverse (l=1)
+ *     1D: 0 centre, 2 neighbours (i+-1), 4 1/centre, 5 coarse inverse
+ *   Values are those of alpha*A_l + mu*M_l (multigrid.py:87-91).
+ * stencil_M / stencil_A: the finest-level M_x / A_x stencils (4 doubles:
+ *   centre, x, y, diagonal; 1D: centre, -, neighbour, -).
+ * temporal: 11 doubles -- M_t (off, main, end), A_t (off, main, end),
+ *   L (off = 0.5, end = 0.5), T_test (1/sqrt h), N_test (sqrt h / 2,
+ *   sqrt(3h)/6) -- see temporal.py:82-144.
+ * wavelet_scale: J doubles, s_j = 2^(j/2) for j = 1..J (wavelet.py:63).
+ */
+typedef struct {
+    int32_t dim;            /* 1 or 2 */
+    int32_t J;              /* N_t = 2^J + 1 */
+    int32_t K;              /* N_x = (2^K - 1)^dim */
+    int32_t vcycles;        /* SolveConfig.vcycles (2) */
+    int32_t smooth;         /* SolveConfig.smooth (3) */
+    int32_t device;         /* CUDA device ordinal */
+    double alpha;           /* SolveConfig.alpha (0.3) */
+    const double *coef;     /* host, see above */
+    const double *stencil_M;
+    const double *stencil_A;
+    const double *temporal;
+    const double *wavelet_scale;
+} hwg_desc;
+
+typedef struct hwg_ctx hwg_ctx;
+
+/* PCG statistics (PCGResult, solver.py:140-148).  Arrays are host buffers
+ * of capacity max_iterations + 1 supplied by the caller (may be NULL). */
+typedef struct {
+    int32_t iterations;
+    int32_t capacity;
+    double *residual_norms;   /* sqrt(rho_k), k = 0..iterations */
+    double *alphas;           /* cg_alphas, iterations entries */
+    double *betas;            /* cg_betas */
+    double ms_schur, ms_precond, ms_vector, ms_total;  /* wall_times */
+    double epsilon_used;      /* the absolute tolerance actually applied */
+} hwg_pcg_stats;
+
+/* Library / context lifetime. */
+const char *hwg_last_error(void);
+int hwg_version(void);
+int hwg_create(const hwg_desc *desc, hwg_ctx **ctx);
+int hwg_destroy(hwg_ctx *ctx);
+/* Device bytes the context holds (workspaces only). */
+int64_t hwg_workspace_bytes(const hwg_ctx *ctx);
+
+/*
+ * WaveletTransform.apply_array / transpose_apply_array (wavelet.py:114-149):
+ * Y = (W_t (x) Id) X, or its transpose.  X, Y: (N_t, N_x); may not alias.
+ */
+int hwg_wavelet(hwg_ctx *ctx, const double *X, double *Y, int transpose, void *stream);
+
+/*
+ * Spatial factor on every row (system.py:48-51 `_spatial`, csr_rows_matvec
+ * _kernels.py:25-34): Y[r] = M_x X[r] (which = 0) or A_x X[r] (which = 1).
+ */
+int hwg_spatial(hwg_ctx *ctx, int which, const double *X, double *Y, int64_t rows, void *stream);
+
+/* SchurOperator.apply_array, five-term form (system.py:116-147, 182-187). */
+int hwg_schur_apply(hwg_ctx *ctx, const double *X, double *Y, void *stream);
+
+/* PreconditionerKX.apply_array (system.py:252-276). */
+int hwg_kx_apply(hwg_ctx *ctx, const double *X, double *Y, void *stream);
+
+/*
+ * Batched V-cycles, MultigridSolver.apply_rows / apply_rows_indexed
+ * (multigrid.py:58-68, _kernels.py:110-249): X[r] = MG_op(r)(B[r]) for
+ * r in [0, rows).  op_host == NULL: every row uses operator `op`
+ * (0 = K_x, 1 + j = C_j); otherwise op_host[r] (host int32 array) picks the
+ * operator per row.  B and X must not alias.
+ */
+int hwg_mg_rows(hwg_ctx *ctx, int32_t op, const int32_t *op_host, const double *B,
+                double *X, int64_t rows, void *stream);
+
+/*
+ * Right-hand side from nodal forcing (system.py:295-324 assemble_rhs with
+ * the P1 x P1 interpolant load (N (x) M_x) F):
+ *   fhat = W^T( B^T K_Y (N (x) M_x) F + e_0 (x) u0proj ).
+ * F: (N_t, N_x) device or NULL (no forcing); u0proj: N_x device moments
+ * <u0, phi_i> or NULL.  load: alternatively an already assembled test-space
+ * load (2*2^J, N_x) on the device (pass F = NULL), e.g. from assemble_load
+ * (spatial.py:269-300) for a callable forcing.
+ */
+int hwg_rhs(hwg_ctx *ctx, const double *F, const double *load, const double *u0proj,
+            double *fhat, void *stream);
+
+/* Deterministic inner product (solver.py:111-129): per-row partials, then
+ * the fixed pairwise tree over rows.  Synchronises `stream`. */
+int hwg_dot(hwg_ctx *ctx, const double *X, const double *Y, int64_t rows, double *result_host,
+            void *stream);
+
+/*
+ * pcg (solver.py:181-263) on S-hat w = fhat, preconditioned by K_X.
+ * Stops when r^T K_X r <= eps^2 with eps = epsilon (absolute) or, if
+ * rtol > 0, eps = rtol * sqrt(f^T K_X f).  w is overwritten (zero start).
+ * Returns HWG_EMAXIT after max_iterations (stats hold the history),
+ * HWG_ENOTSPD if p^T S p <= 0, HWG_EINVAL if the tolerance is not positive.
+ */
+int hwg_pcg(hwg_ctx *ctx, const double *fhat, double *w, double epsilon, double rtol,
+            int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *stats,
+            void *stream);
+
+/*
+ * End-to-end call for host buffers (the e2e leg of bench.py): copies fhat
+ * from host memory, solves with hwg_pcg, applies u = W w and copies u back.
+ */
+int hwg_solve_host(hwg_ctx *ctx, const double *fhat_host, double *u_host, double epsilon,
+                   double rtol, int32_t max_iterations, int32_t recompute_every,
+                   hwg_pcg_stats *stats, void *stream);
+
+/* Kernel launches issued by this context since creation (bench evidence). */
+int64_t hwg_launch_count(const hwg_ctx *ctx);
+
+/*
+ * Per-kernel-class timing for bench.py's roofline: CUDA events are recorded
+ * on the launching stream around every multigrid launch while enabled
+ * (enable != 0 also resets the totals).  Classes: 0 mg2d_stream DOWN on the
+ * finest level, 1 mg2d_stream UP on the finest level, 2 DOWN on coarser
+ * levels, 3 UP on coarser levels, 4 mg2d_coarse, 5 mg1d.  `bytes` is the
+ * algorithmic HBM traffic of those launches (each input read once, each
+ * output written once).  hwg_profile_read synchronises the context's events.
+ */
+int hwg_profile_enable(hwg_ctx *ctx, int enable);
+int hwg_profile_read(hwg_ctx *ctx, int kclass, double *ms, double *bytes, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEATWAVE_B200_H */

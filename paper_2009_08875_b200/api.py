@@ -1,0 +1,602 @@
+"""The reference's Python solver API, backed by the B200 kernels.
+
+Drop-in for ``heatwave`` (/root/reference/pkg/src/heatwave/__init__.py:
+12-28) on the hot path: ``assemble_system``, ``SchurOperator.apply_array``,
+``PreconditionerKX.apply_array``, ``WaveletTransform.apply_array`` /
+``transpose_apply_array``, ``MultigridSolver.apply*``, ``pcg`` and
+``solve_heat`` keep their names, arguments, return types and exceptions.
+Arrays may be numpy (copied to the GPU and back, as a drop-in would) or
+CUDA ``torch`` tensors (kept on the device).  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import discretization as disc
+from ._lib import IterationLimitError, check as _check
+from .device import GpuContext, as_device, _torch
+from .discretization import ProblemData, FineMesh
+
+__all__ = [
+    "SolveConfig", "SpaceTimeVector", "TemporalDiscretization", "MeshHierarchy",
+    "build_mesh_hierarchy", "WaveletTransform", "MultigridSolver", "make_solver",
+    "SchurOperator", "PreconditionerKX", "RightHandSide", "ProblemAssembly",
+    "assemble_system", "PCGResult", "IterationLimitError", "pcg", "solve_heat",
+    "HeatSolution", "measure_error", "estimate_condition", "lanczos_tridiagonal",
+    "ParallelPlan", "split_ranges", "tree_reduce", "ProblemData", "project_initial",
+    "decaying_heat", "forced_heat", "PROBLEMS",
+]
+
+
+# --------------------------------------------------------------------------
+# containers (sparse.py:132-175, solver.py:34-80, temporal.py:21-49)
+# --------------------------------------------------------------------------
+@dataclass
+class SolveConfig:
+    alpha: float = 0.3
+    epsilon: float = 1e-6
+    vcycles: int = 2
+    smooth: int = 3
+    workers: int = 1
+    exact_inverses: bool = False
+    max_iterations: int = 200
+    recompute_every: int = 50
+    form: str = "five_term"
+    device: int = 0
+
+
+class SpaceTimeVector:
+    """(n_t, n_x) coefficient array; numpy on the host or a CUDA tensor."""
+
+    def __init__(self, array):
+        torch = _torch()
+        if isinstance(array, torch.Tensor):
+            if array.dim() != 2:
+                raise ValueError("SpaceTimeVector needs a 2-d coefficient array")
+            self.array = array.to(dtype=torch.float64).contiguous()
+        else:
+            self.array = np.ascontiguousarray(array, dtype=float)
+            if self.array.ndim != 2:
+                raise ValueError("SpaceTimeVector needs a 2-d coefficient array")
+
+    @classmethod
+    def zeros(cls, n_t, n_x):
+        return cls(np.zeros((n_t, n_x)))
+
+    @property
+    def n_t(self):
+        return self.array.shape[0]
+
+    @property
+    def n_x(self):
+        return self.array.shape[1]
+
+    def numpy(self):
+        a = self.array
+        return a if isinstance(a, np.ndarray) else a.detach().cpu().numpy()
+
+    def vec(self):
+        return self.numpy().reshape(-1).copy()
+
+    def copy(self):
+        a = self.array
+        return SpaceTimeVector(a.copy() if isinstance(a, np.ndarray) else a.clone())
+
+    def norm(self):
+        return float(np.linalg.norm(self.numpy()))
+
+
+@dataclass(frozen=True)
+class TemporalDiscretization:
+    J: int
+
+    def __post_init__(self):
+        if self.J < 0:
+            raise ValueError("refinement level J must be >= 0")
+
+    @property
+    def n_elements(self):
+        return 2 ** self.J
+
+    @property
+    def N_t(self):
+        return 2 ** self.J + 1
+
+    @property
+    def mesh_width(self):
+        return 2.0 ** -self.J
+
+    def nodes(self):
+        return np.linspace(0.0, 1.0, self.N_t)
+
+
+class MeshHierarchy:
+    """Nested uniform meshes of [0,1]^d, levels 1..K (spatial.py:73-95)."""
+
+    def __init__(self, d, K):
+        if d not in (1, 2, 3):
+            raise ValueError("dimension must be 1, 2 or 3")
+        if K < 1:
+            raise ValueError("finest level K must be >= 1")
+        if d == 3:
+            raise NotImplementedError("the GPU path implements d = 1 and d = 2")
+        self.d, self.K = d, K
+        self._finest = None
+
+    @property
+    def finest(self) -> FineMesh:
+        if self._finest is None:
+            self._finest = FineMesh(self.d, self.K)
+        return self._finest
+
+    @property
+    def N_x(self):
+        return (2 ** self.K - 1) ** self.d
+
+
+def build_mesh_hierarchy(d: int, K: int) -> MeshHierarchy:
+    return MeshHierarchy(d, K)
+
+
+def project_initial(mesh: FineMesh, u0):
+    return disc.project_initial(mesh, u0)
+
+
+# --------------------------------------------------------------------------
+# helpers: numpy/tensor in, same kind out
+# --------------------------------------------------------------------------
+def _in(ctx, X, shape=None):
+    t, host = as_device(X, ctx.device)
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t, host
+
+
+def _out(ctx, result, host, out):
+    """Deliver a device result as numpy (host input) or tensor, honouring out=."""
+    torch = _torch()
+    if out is not None:
+        if isinstance(out, torch.Tensor):
+            out.copy_(result)
+        else:
+            out[...] = result.cpu().numpy()
+        return out
+    return result.cpu().numpy() if host else result
+
+
+# --------------------------------------------------------------------------
+# wavelet transform (wavelet.py:99-149)
+# --------------------------------------------------------------------------
+class WaveletTransform:
+    """W_t (x) Id_x on the GPU (J lifting stages per application)."""
+
+    def __init__(self, ctx: GpuContext):
+        self.ctx = ctx
+        self.level_of = disc.level_of(ctx.J)
+
+    @property
+    def J(self):
+        return self.ctx.J
+
+    def _apply(self, X, transpose, out):
+        torch = _torch()
+        if X.shape[0] != self.ctx.n_t:
+            raise ValueError(f"expected {self.ctx.n_t} temporal rows, got {X.shape[0]}")
+        x, host = _in(self.ctx, X, (self.ctx.n_t, self.ctx.n_x))
+        y = torch.empty_like(x)
+        self.ctx.wavelet(x, y, transpose)
+        return _out(self.ctx, y, host, out)
+
+    def apply_array(self, X, pool=None, out=None, scratch=None):
+        return self._apply(X, False, out)
+
+    def transpose_apply_array(self, X, pool=None, out=None, scratch=None):
+        return self._apply(X, True, out)
+
+
+# --------------------------------------------------------------------------
+# multigrid (multigrid.py:31-131)
+# --------------------------------------------------------------------------
+class MultigridSolver:
+    """n_vcycles V-cycles of alpha*A_x + mu*M_x on every given row."""
+
+    thread_safe = True
+
+    def __init__(self, ctx: GpuContext, op: int, alpha: float, mu: float,
+                 n_vcycles: int = 2, n_smooth: int = 3, hierarchy=None):
+        self.ctx, self.op = ctx, op
+        self.alpha, self.mu = alpha, mu
+        self.n_vcycles, self.n_smooth = n_vcycles, n_smooth
+        self.hierarchy = hierarchy
+
+    @property
+    def n(self):
+        return self.ctx.n_x
+
+    def _rows(self, B):
+        torch = _torch()
+        b, host = _in(self.ctx, B)
+        if b.dim() != 2 or b.shape[1] != self.n:
+            raise ValueError(f"right-hand side rows must have length {self.n}")
+        x = torch.empty_like(b)
+        if b.shape[0]:
+            self.ctx.mg_rows(self.op, b, x)
+        return x, host
+
+    def apply(self, b):
+        b = np.ascontiguousarray(b, dtype=float) if not hasattr(b, "device") else b
+        if tuple(b.shape) != (self.n,):
+            raise ValueError(f"right-hand side must have length {self.n}")
+        x, host = self._rows(b.reshape(1, -1))
+        return x[0].cpu().numpy() if host else x[0]
+
+    __call__ = apply
+
+    def apply_rows(self, B, out, r0, r1):
+        x, host = self._rows(B[r0:r1])
+        _out_rows(out, r0, r1, x)
+
+    def apply_rows_indexed(self, B, out, rows):
+        rows = np.asarray(rows, dtype=np.int64)
+        x, host = self._rows(B[rows] if isinstance(B, np.ndarray) else B[_torch().as_tensor(rows, device=B.device)])
+        torch = _torch()
+        if isinstance(out, torch.Tensor):
+            out[torch.as_tensor(rows, device=out.device)] = x
+        else:
+            out[rows] = x.cpu().numpy()
+
+    def solve_into(self, b, x):
+        x[...] = self.apply(b)
+
+
+def _out_rows(out, r0, r1, x):
+    torch = _torch()
+    if isinstance(out, torch.Tensor):
+        out[r0:r1] = x
+    else:
+        out[r0:r1] = x.cpu().numpy()
+
+
+def make_solver(hierarchy: MeshHierarchy, alpha: float, mu: float, n_vcycles: int = 2,
+                n_smooth: int = 3, level_operators=None, D=None, c=0.0,
+                device: int = 0) -> MultigridSolver:
+    """A standalone batched MG solver (its own small context, one operator)."""
+    if alpha <= 0 and mu <= 0:
+        raise ValueError("need alpha > 0 or mu > 0")
+    d, K = hierarchy.d, hierarchy.K
+    # every operator slot of this small (J = 1) context is (alpha, mu)
+    table = np.zeros((3, K + 1, disc.COEF_STRIDE))
+    for l in range(1, K + 1):
+        M, A = disc.level_stencils(d, l, D, c)
+        vals = {k: alpha * A.get(k, 0.0) + mu * M.get(k, 0.0) for k in ("c0", "cx", "cy", "cd")}
+        c0 = vals["c0"]
+        table[:, l, :6] = [c0, vals["cx"], vals["cy"], vals["cd"], 1.0 / c0,
+                           1.0 / c0 if l == 1 else 0.0]
+    ctx = GpuContext(d, 1, K, alpha, n_vcycles, n_smooth, D, c, device, coef=table)
+    return MultigridSolver(ctx, 0, alpha, mu, n_vcycles, n_smooth, hierarchy)
+
+
+# --------------------------------------------------------------------------
+# the preconditioned Schur system (system.py:67-324)
+# --------------------------------------------------------------------------
+class SchurOperator:
+    """S-hat = W^T S W (five-term form) as a matrix-free GPU operator."""
+
+    def __init__(self, ctx: GpuContext, form="five_term"):
+        if form not in ("test_space", "five_term"):
+            raise ValueError("form must be 'five_term' or 'test_space'")
+        if form == "test_space":
+            raise NotImplementedError("the GPU path implements the production five-term form")
+        self.ctx = ctx
+        self.form = form
+
+    @property
+    def n_t(self):
+        return self.ctx.n_t
+
+    @property
+    def n_x(self):
+        return self.ctx.n_x
+
+    def apply_array(self, X, pool=None, out=None):
+        torch = _torch()
+        x, host = _in(self.ctx, X, (self.n_t, self.n_x))
+        y = torch.empty_like(x)
+        self.ctx.schur(x, y)
+        return _out(self.ctx, y, host, out)
+
+    def apply(self, v: SpaceTimeVector, pool=None) -> SpaceTimeVector:
+        if tuple(v.array.shape) != (self.n_t, self.n_x):
+            raise ValueError(f"expected shape ({self.n_t}, {self.n_x}), got {tuple(v.array.shape)}")
+        return SpaceTimeVector(self.apply_array(v.array, pool))
+
+
+class PreconditionerKX:
+    """K_X = blockdiag[C_|lambda| A_x C_|lambda|] over wavelet coordinates."""
+
+    def __init__(self, ctx: GpuContext, blocks: dict):
+        self.ctx = ctx
+        self.blocks = blocks
+        self.level_of = disc.level_of(ctx.J)
+        self.alpha = ctx.alpha
+
+    def apply_array(self, X, pool=None, out=None):
+        for lvl in np.unique(self.level_of[: X.shape[0]]):
+            if int(lvl) not in self.blocks:
+                raise KeyError(f"no preconditioner block for level {int(lvl)}")
+        torch = _torch()
+        x, host = _in(self.ctx, X, (self.ctx.n_t, self.ctx.n_x))
+        y = torch.empty_like(x)
+        self.ctx.kx(x, y)
+        return _out(self.ctx, y, host, out)
+
+    def apply(self, v: SpaceTimeVector, pool=None) -> SpaceTimeVector:
+        return SpaceTimeVector(self.apply_array(v.array, pool))
+
+
+class RightHandSide:
+    """f-hat = W^T (B^T K_Y g + u0); the two parts are formed on demand."""
+
+    def __init__(self, ctx, f_hat, g_source=None, u0proj=None):
+        self.ctx = ctx
+        self.f_hat = f_hat
+        self._g_source = g_source      # ("F", tensor) or ("load", tensor) or None
+        self._u0proj = u0proj
+        self._g = self._u = None
+
+    def _part(self, which):
+        torch = _torch()
+        out = torch.empty((self.ctx.n_t, self.ctx.n_x), dtype=torch.float64, device=self.ctx.device)
+        if which == "g":
+            kind, t = self._g_source if self._g_source else (None, None)
+            self.ctx.rhs(t if kind == "F" else None, t if kind == "load" else None, None, out)
+        else:
+            self.ctx.rhs(None, None, self._u0proj, out)
+        return SpaceTimeVector(out if not isinstance(self.f_hat.array, np.ndarray) else out.cpu().numpy())
+
+    @property
+    def g_part(self):
+        if self._g is None:
+            self._g = self._part("g")
+        return self._g
+
+    @property
+    def u0_part(self):
+        if self._u is None:
+            self._u = self._part("u")
+        return self._u
+
+
+def assemble_rhs(ctx: GpuContext, problem: ProblemData, mesh: FineMesh, forcing=None,
+                 host=True) -> RightHandSide:
+    """f-hat on the GPU.  ``forcing`` = nodal values F (N_t, N_x) of the
+    P1 x P1 forcing interpolant (load (N (x) M_x) F); otherwise problem.g is
+    integrated on the host (assemble_load) and the rest runs on the GPU."""
+    torch = _torch()
+    src = None
+    if forcing is not None:
+        F, _ = _in(ctx, forcing, (ctx.n_t, ctx.n_x))
+        src = ("F", F)
+    elif problem.g is not None:
+        load = disc.assemble_load(mesh, ctx.J, problem.g)
+        src = ("load", _in(ctx, load)[0])
+    u0 = torch.from_numpy(np.ascontiguousarray(disc.project_initial(mesh, problem.u0))).to(ctx.device)
+    fhat = torch.empty((ctx.n_t, ctx.n_x), dtype=torch.float64, device=ctx.device)
+    if src is None:
+        ctx.rhs(None, None, u0, fhat)
+    else:
+        ctx.rhs(src[1] if src[0] == "F" else None, src[1] if src[0] == "load" else None, u0, fhat)
+    f = SpaceTimeVector(fhat.cpu().numpy() if host else fhat)
+    return RightHandSide(ctx, f, src, u0)
+
+
+@dataclass
+class ProblemAssembly:
+    temporal_disc: TemporalDiscretization
+    temporal: object
+    test: object
+    hierarchy: MeshHierarchy
+    spatial: object
+    wavelet: WaveletTransform
+    K_x: MultigridSolver
+    S: SchurOperator
+    K_X: PreconditionerKX
+    rhs: RightHandSide
+    ctx: GpuContext = None
+
+
+def assemble_system(problem: ProblemData, J: int, K: int, config: SolveConfig = None,
+                    forcing=None, host_rhs=True) -> ProblemAssembly:
+    """Assemble the GPU system (solver.py:353-386).
+
+    Extensions: ``forcing`` -- nodal forcing values F (the BASELINE recipe);
+    ``host_rhs=False`` keeps f-hat on the device as a CUDA tensor."""
+    config = config or SolveConfig()
+    if config.exact_inverses:
+        raise NotImplementedError("exact (sparse-LU) inner inverses stay on the CPU reference")
+    d = problem.D.shape[0]
+    hier = build_mesh_hierarchy(d, K)
+    ctx = GpuContext(d, J, K, config.alpha, config.vcycles, config.smooth, problem.D,
+                     problem.c, config.device)
+    wt = WaveletTransform(ctx)
+    K_x = MultigridSolver(ctx, 0, 1.0, 0.0, config.vcycles, config.smooth, hier)
+    blocks = {j: MultigridSolver(ctx, 1 + j, config.alpha, 2.0 ** j, config.vcycles,
+                                 config.smooth, hier) for j in range(J + 1)}
+    S = SchurOperator(ctx, config.form)
+    KX = PreconditionerKX(ctx, blocks)
+    rhs = assemble_rhs(ctx, problem, hier.finest, forcing, host_rhs)
+    return ProblemAssembly(TemporalDiscretization(J), disc.temporal_values(J), None, hier,
+                           (ctx.stencil_M, ctx.stencil_A), wt, K_x, S, KX, rhs, ctx)
+
+
+# --------------------------------------------------------------------------
+# PCG (solver.py:111-263)
+# --------------------------------------------------------------------------
+@dataclass
+class ParallelPlan:
+    """Accepted for signature compatibility; one GPU runs every row."""
+
+    n_workers: int
+    column_ranges: tuple
+    halo_width: int
+    reduction: str = "tree"
+
+    @classmethod
+    def create(cls, n_workers: int, n_columns: int, halo_width: int = 2):
+        return cls(n_workers, tuple(split_ranges(n_columns, n_workers)), halo_width)
+
+    def validate(self):
+        prev = 0
+        for (a, b) in self.column_ranges:
+            if a != prev:
+                raise ValueError("ranges must be disjoint and contiguous")
+            prev = b
+        return self
+
+
+def split_ranges(n, parts):
+    out, (base, extra), start = [], divmod(n, parts), 0
+    for w in range(parts):
+        stop = start + base + (1 if w < extra else 0)
+        if stop > start:
+            out.append((start, stop))
+        start = stop
+    return out
+
+
+def tree_reduce(values):
+    """Fixed-order pairwise summation (the device uses the same tree)."""
+    buf = np.asarray(values, dtype=float)
+    while buf.size > 1:
+        half = buf.size // 2
+        s = buf[: 2 * half: 2] + buf[1: 2 * half: 2]
+        buf = np.concatenate([s, buf[2 * half:]]) if buf.size % 2 else s
+    return float(buf[0])
+
+
+@dataclass
+class PCGResult:
+    w: SpaceTimeVector
+    iterations: int
+    residual_norms: list
+    kappa_estimate: Optional[float]
+    wall_times: dict
+    cg_alphas: list = field(default_factory=list)
+    cg_betas: list = field(default_factory=list)
+
+
+def lanczos_tridiagonal(alphas, betas):
+    n = len(alphas)
+    d = np.zeros(n)
+    e = np.zeros(max(n - 1, 0))
+    for k in range(n):
+        d[k] = 1.0 / alphas[k] + (betas[k - 1] / alphas[k - 1] if k > 0 else 0.0)
+        if k < n - 1:
+            e[k] = np.sqrt(max(betas[k], 0.0)) / alphas[k]
+    return d, e
+
+
+def _kappa_from_cg(alphas, betas):
+    if len(alphas) < 2:
+        return None
+    d, e = lanczos_tridiagonal(alphas, betas)
+    ev = np.linalg.eigvalsh(np.diag(d) + np.diag(e, 1) + np.diag(e, -1))
+    return float(ev[-1] / ev[0])
+
+
+def estimate_condition(result: PCGResult) -> float:
+    if result.iterations < 5:
+        raise ValueError("need at least 5 recorded iterations for a condition estimate")
+    return _kappa_from_cg(result.cg_alphas, result.cg_betas)
+
+
+def pcg(S: SchurOperator, K: PreconditionerKX, f_hat, epsilon: float,
+        plan: Optional[ParallelPlan] = None, max_iterations: int = 200,
+        recompute_every: int = 50, rtol: float = 0.0) -> PCGResult:
+    """PCG on S-hat w = f-hat, stopping on r^T K_X r <= eps^2 (device-resident).
+
+    Extension: ``rtol > 0`` stops on sqrt(r^T K_X r) <= rtol sqrt(f^T K_X f)
+    (the BASELINE rule); ``epsilon`` is then ignored."""
+    torch = _torch()
+    if not (epsilon > 0) and not (rtol > 0):
+        raise ValueError("tolerance must be positive")
+    if S.ctx is not K.ctx:
+        raise ValueError("S and K_X must come from the same assembled system")
+    ctx = S.ctx
+    fv = f_hat.f_hat if isinstance(f_hat, RightHandSide) else f_hat
+    f, host = _in(ctx, fv.array, (ctx.n_t, ctx.n_x))
+    w = torch.empty_like(f)
+    t0 = time.perf_counter()
+    stats, rc = ctx.pcg(f, w, epsilon, rtol, max_iterations, recompute_every)
+    times = {"schur": stats["ms_schur"] / 1e3, "precond": stats["ms_precond"] / 1e3,
+             "vector": stats["ms_vector"] / 1e3, "total": time.perf_counter() - t0}
+    _check(rc, stats["residual_norms"])
+    k = stats["iterations"]
+    kappa = _kappa_from_cg(stats["alphas"], stats["betas"]) if k >= 5 else None
+    wv = SpaceTimeVector(w.cpu().numpy() if host else w)
+    return PCGResult(wv, k, stats["residual_norms"], kappa, times, stats["alphas"],
+                     stats["betas"])
+
+
+@dataclass
+class HeatSolution:
+    coefficients: SpaceTimeVector
+    mesh: FineMesh
+    temporal: TemporalDiscretization
+    algebraic_error: float
+
+    def trace_coefficients(self, t: float) -> np.ndarray:
+        if not 0.0 <= t <= 1.0:
+            raise ValueError("time must lie in [0, T] = [0, 1]")
+        X = self.coefficients.numpy()
+        pos = t * self.temporal.n_elements
+        k = min(int(pos), self.temporal.n_elements - 1)
+        s = pos - k
+        return (1.0 - s) * X[k] + s * X[k + 1]
+
+
+def measure_error(solution: HeatSolution, exact, t: float) -> float:
+    coeffs = solution.trace_coefficients(t)
+    return disc.l2_error_on_mesh(solution.mesh, coeffs, lambda x: exact(t, x))
+
+
+def solve_heat(problem: ProblemData, J: int, K: int, config: SolveConfig = None,
+               forcing=None):
+    """Assemble, run PCG, return (PCGResult, HeatSolution) (solver.py:389-403)."""
+    config = config or SolveConfig()
+    asm = assemble_system(problem, J, K, config, forcing)
+    result = pcg(asm.S, asm.K_X, asm.rhs, config.epsilon, None, config.max_iterations,
+                 config.recompute_every)
+    u = asm.wavelet.apply_array(result.w.array)
+    sol = HeatSolution(SpaceTimeVector(u), asm.hierarchy.finest, asm.temporal_disc,
+                       result.residual_norms[-1])
+    return result, sol
+
+
+# --------------------------------------------------------------------------
+# manufactured problems (problems.py:14-44)
+# --------------------------------------------------------------------------
+def _prod_sines(pts):
+    return np.prod(np.sin(np.pi * pts), axis=1)
+
+
+def decaying_heat(d: int) -> ProblemData:
+    rate = d * np.pi ** 2
+    return ProblemData(D=np.eye(d), c=0.0, u0=_prod_sines, g=None,
+                       exact_solution=lambda t, pts: np.exp(-rate * t) * _prod_sines(pts))
+
+
+def forced_heat(d: int) -> ProblemData:
+    factor = d * np.pi ** 2 - 1.0
+    return ProblemData(D=np.eye(d), c=0.0, u0=_prod_sines,
+                       g=lambda t, pts: factor * np.exp(-t) * _prod_sines(pts),
+                       exact_solution=lambda t, pts: np.exp(-t) * _prod_sines(pts))
+
+
+PROBLEMS = {"decaying": decaying_heat, "forced": forced_heat}

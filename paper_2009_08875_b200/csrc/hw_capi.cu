@@ -1,0 +1,753 @@
+// hw_capi.cu -- C ABI (include/heatwave_b200.h): context, operator
+// orchestration and the device-resident PCG driver.
+//
+// Each entry point replaces one call site of the reference package
+// (/root/reference/pkg/src/heatwave): see the header for the mapping.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/heatwave_b200.h"
+#include "hw_common.cuh"
+
+#include "hw_internal.cuh"
+
+using namespace hw;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? HWG_ENOMEM : HWG_ECUDA,         \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+#define TRY(expr)                \
+    do {                         \
+        int rc_ = (expr);        \
+        if (rc_ != HWG_OK) return rc_; \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct DevBand {           // a temporal factor in CSR on the device
+    int32_t *ip = nullptr, *ix = nullptr;
+    double *v = nullptr;
+    TCsr view() const { return TCsr{ip, ix, v}; }
+};
+
+struct hwg_ctx {
+    hwg_desc d{};
+    int dim = 2, J = 0, K = 0, m = 0, nv = 2;
+    int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx
+    int64_t rows_max = 0;              // MG batch capacity (rows)
+    Grid grid{};
+    Stencil SM{}, SA{};
+    std::vector<double> coef_host;
+    std::vector<double> scale;         // wavelet s_j
+    double *coef = nullptr;            // device table
+    int32_t *row_op_kx = nullptr;      // device: 1 + level_of[r]
+    std::vector<int32_t> level_of;
+    DevBand At, Mt, L, LT, T, TT, Nn, NT;
+    // workspaces
+    double *U = nullptr, *MxU = nullptr, *AxU = nullptr, *T12 = nullptr, *G12 = nullptr;
+    std::vector<double *> mgX, mgB;    // per level 1..K-1 (2D streaming + coarse)
+    double *part = nullptr, *tmp = nullptr, *scal = nullptr;
+    int *flag = nullptr;
+    double *hscal = nullptr;           // pinned host mirror of scalars
+    // PCG vectors (lazy)
+    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double *fdev = nullptr, *wdev = nullptr;
+    int64_t bytes = 0;
+    int64_t launches = 0;
+    std::vector<void *> allocs;
+    // roofline profiling (hwg_profile_*)
+    bool prof = false;
+    struct ProfRec { cudaEvent_t a, b; int cls; double bytes; };
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> prof_pool;
+    double prof_ms[6] = {0}, prof_bytes[6] = {0};
+    int64_t prof_n[6] = {0};
+};
+
+static cudaEvent_t prof_event(hwg_ctx *c)
+{
+    if (!c->prof_pool.empty()) {
+        cudaEvent_t e = c->prof_pool.back();
+        c->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// drain recorded event pairs into the per-class totals
+static void prof_flush(hwg_ctx *c)
+{
+    for (auto &r : c->prof_recs) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        c->prof_ms[r.cls] += ms;
+        c->prof_bytes[r.cls] += r.bytes;
+        c->prof_n[r.cls] += 1;
+        c->prof_pool.push_back(r.a);
+        c->prof_pool.push_back(r.b);
+    }
+    c->prof_recs.clear();
+}
+
+struct ProfScope {
+    hwg_ctx *c;
+    cudaStream_t st;
+    int cls;
+    double bytes;
+    cudaEvent_t a{}, b{};
+    ProfScope(hwg_ctx *c_, cudaStream_t s, int k, double by) : c(c_), st(s), cls(k), bytes(by)
+    {
+        if (c->prof) {
+            if (c->prof_recs.size() > 4096) prof_flush(c);
+            a = prof_event(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope()
+    {
+        if (c->prof) {
+            b = prof_event(c);
+            cudaEventRecord(b, st);
+            c->prof_recs.push_back({a, b, cls, bytes});
+        }
+    }
+};
+
+static int dalloc(hwg_ctx *c, double **p, int64_t count)
+{
+    void *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, (size_t)count * sizeof(double));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HWG_ENOMEM, "cudaMalloc of " + std::to_string(count * 8) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+    }
+    c->allocs.push_back(q);
+    c->bytes += count * (int64_t)sizeof(double);
+    *p = (double *)q;
+    return HWG_OK;
+}
+
+template <class T>
+static int upload(hwg_ctx *c, T **dst, const std::vector<T> &src)
+{
+    void *q = nullptr;
+    CK(cudaMalloc(&q, std::max<size_t>(1, src.size()) * sizeof(T)));
+    c->allocs.push_back(q);
+    c->bytes += (int64_t)(src.size() * sizeof(T));
+    if (!src.empty()) CK(cudaMemcpy(q, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    *dst = (T *)q;
+    return HWG_OK;
+}
+
+// CSR rows given as (col, value) lists in ascending column order
+static int make_band(hwg_ctx *c, DevBand *b, const std::vector<std::vector<std::pair<int, double>>> &rows)
+{
+    std::vector<int32_t> ip(1, 0), ix;
+    std::vector<double> v;
+    for (auto &row : rows) {
+        for (auto &e : row) {
+            ix.push_back(e.first);
+            v.push_back(e.second);
+        }
+        ip.push_back((int32_t)ix.size());
+    }
+    TRY(upload(c, &b->ip, ip));
+    TRY(upload(c, &b->ix, ix));
+    TRY(upload(c, &b->v, v));
+    return HWG_OK;
+}
+
+// temporal.py:82-144 with the values computed by the host (desc->temporal)
+static int build_temporal(hwg_ctx *c)
+{
+    const double *t = c->d.temporal;
+    const int n = (int)c->nt;
+    const int ne = n - 1;
+    using Rows = std::vector<std::vector<std::pair<int, double>>>;
+    auto tri = [&](double off_lo, double main, double end, double off_hi, bool drop_zero_main) {
+        Rows rows(n);
+        for (int i = 0; i < n; ++i) {
+            if (i > 0) rows[i].push_back({i - 1, off_lo});
+            double dv = (i == 0 || i == n - 1) ? end : main;
+            if (!(drop_zero_main && dv == 0.0)) rows[i].push_back({i, dv});
+            if (i < n - 1) rows[i].push_back({i + 1, off_hi});
+        }
+        return rows;
+    };
+    // M_t = h tridiag(1/6, 2/3, 1/6), ends h/3
+    Rows Mt = tri(t[0], t[1], t[2], t[0], false);
+    // A_t = tridiag(-1/h, 2/h, -1/h), ends 1/h
+    Rows At = tri(t[3], t[4], t[5], t[3], false);
+    if (n == 1) {  // J = 0 is not reachable (N_t = 2), kept for safety
+        Mt = Rows(1);
+        At = Rows(1);
+    }
+    // L: L[i,i-1] = -1/2, L[i,i+1] = +1/2, L[0,0] = -1/2, L[n-1,n-1] = +1/2
+    Rows L(n), LT(n);
+    for (int i = 0; i < n; ++i) {
+        if (i > 0) L[i].push_back({i - 1, -t[6]});
+        if (i == 0) L[i].push_back({0, -t[7]});
+        if (i == n - 1) L[i].push_back({i, t[7]});
+        if (i < n - 1) L[i].push_back({i + 1, t[6]});
+        // L^T[i,k] = L[k,i]
+        if (i > 0) LT[i].push_back({i - 1, t[6]});
+        if (i == 0) LT[i].push_back({0, -t[7]});
+        if (i == n - 1) LT[i].push_back({i, t[7]});
+        if (i < n - 1) LT[i].push_back({i + 1, -t[6]});
+    }
+    // test matrices (2*ne rows): T[2k,k] = -1/sqrt h, T[2k,k+1] = 1/sqrt h,
+    // odd rows of T eliminated; N[2k,k] = N[2k,k+1] = sqrt h/2,
+    // N[2k+1,k] = -sqrt(3h)/6, N[2k+1,k+1] = +sqrt(3h)/6
+    Rows T(2 * ne), Nn(2 * ne), TT(n), NT(n);
+    for (int k = 0; k < ne; ++k) {
+        T[2 * k] = {{k, -t[8]}, {k + 1, t[8]}};
+        Nn[2 * k] = {{k, t[9]}, {k + 1, t[9]}};
+        Nn[2 * k + 1] = {{k, -t[10]}, {k + 1, t[10]}};
+    }
+    for (int i = 0; i < n; ++i) {
+        // T^T row i: (2(i-1), +1/sqrt h), (2i, -1/sqrt h)
+        if (i > 0) TT[i].push_back({2 * (i - 1), t[8]});
+        if (i < ne) TT[i].push_back({2 * i, -t[8]});
+        // N^T row i: (2i-2, N[2i-2,i]), (2i-1, N[2i-1,i]), (2i, N[2i,i]), (2i+1, N[2i+1,i])
+        if (i > 0) {
+            NT[i].push_back({2 * (i - 1), t[9]});
+            NT[i].push_back({2 * (i - 1) + 1, t[10]});
+        }
+        if (i < ne) {
+            NT[i].push_back({2 * i, t[9]});
+            NT[i].push_back({2 * i + 1, -t[10]});
+        }
+    }
+    TRY(make_band(c, &c->Mt, Mt));
+    TRY(make_band(c, &c->At, At));
+    TRY(make_band(c, &c->L, L));
+    TRY(make_band(c, &c->LT, LT));
+    TRY(make_band(c, &c->T, T));
+    TRY(make_band(c, &c->TT, TT));
+    TRY(make_band(c, &c->Nn, Nn));
+    TRY(make_band(c, &c->NT, NT));
+    return HWG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// multigrid driver
+// ---------------------------------------------------------------------------
+static int64_t level_size(const hwg_ctx *c, int l)
+{
+    const int64_t m = (1LL << l) - 1;
+    return c->dim == 2 ? m * m : m;
+}
+
+// X[r] = MG_op(B[r]) for rows [0, rows); row_op: device per-row operator or null
+static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op,
+                    const int32_t *row_op, cudaStream_t st)
+{
+    for (int64_t r0 = 0; r0 < rows; r0 += c->rows_max) {
+        const int64_t nr = std::min<int64_t>(c->rows_max, rows - r0);
+        const double *Bp = B + r0 * c->nx;
+        double *Xp = X + r0 * c->nx;
+        const int32_t *ro = row_op ? row_op + r0 : nullptr;
+        if (c->dim == 1) {
+            Mg1dArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, ro, op, nr};
+            ProfScope ps(c, st, 5, 16.0 * nr * c->nx);
+            CK(mg1d_launch(a, st));
+            ++c->launches;
+            continue;
+        }
+        if (c->K <= kCoarseTop2d) {
+            MgCoarseArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, 1, ro, op, nr};
+            ProfScope ps(c, st, 4, 16.0 * nr * c->nx);
+            CK(mg2d_coarse_launch(a, st));
+            ++c->launches;
+            continue;
+        }
+        for (int cyc = 0; cyc < c->nv; ++cyc) {
+            for (int l = c->K; l > kCoarseTop2d; --l) {
+                MgStreamArgs a{};
+                a.B = (l == c->K) ? Bp : c->mgB[l];
+                a.ldB = level_size(c, l);
+                a.X = (l == c->K) ? Xp : c->mgX[l];
+                a.ldX = level_size(c, l);
+                a.Bc = c->mgB[l - 1];
+                a.ldBc = level_size(c, l - 1);
+                a.coef = c->coef;
+                a.levels_p1 = c->K + 1;
+                a.level = l;
+                a.n = (1 << l) - 1;
+                a.row_op = ro;
+                a.op = op;
+                a.zero_start = (l < c->K || cyc == 0) ? 1 : 0;
+                const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
+                ProfScope ps(c, st, l == c->K ? 0 : 2,
+                             8.0 * nr * (n2 * (a.zero_start ? 2 : 3) + m2));
+                CK(mg2d_stream_launch(a, true, nr, st));
+                ++c->launches;
+            }
+            MgCoarseArgs ca{c->mgB[kCoarseTop2d], level_size(c, kCoarseTop2d),
+                            c->mgX[kCoarseTop2d], level_size(c, kCoarseTop2d), c->coef,
+                            c->K + 1, kCoarseTop2d, 1, 1, ro, op, nr};
+            {
+                ProfScope ps(c, st, 4, 16.0 * nr * level_size(c, kCoarseTop2d));
+                CK(mg2d_coarse_launch(ca, st));
+            }
+            ++c->launches;
+            for (int l = kCoarseTop2d + 1; l <= c->K; ++l) {
+                MgStreamArgs a{};
+                a.B = (l == c->K) ? Bp : c->mgB[l];
+                a.ldB = level_size(c, l);
+                a.X = (l == c->K) ? Xp : c->mgX[l];
+                a.ldX = level_size(c, l);
+                a.Xc = c->mgX[l - 1];
+                a.ldXc = level_size(c, l - 1);
+                a.coef = c->coef;
+                a.levels_p1 = c->K + 1;
+                a.level = l;
+                a.n = (1 << l) - 1;
+                a.row_op = ro;
+                a.op = op;
+                const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
+                ProfScope ps(c, st, l == c->K ? 1 : 3, 8.0 * nr * (3 * n2 + m2));
+                CK(mg2d_stream_launch(a, false, nr, st));
+                ++c->launches;
+            }
+        }
+    }
+    return HWG_OK;
+}
+
+static int wavelet(hwg_ctx *c, const double *X, double *Y, double *S1, double *S2, bool tr,
+                   cudaStream_t st)
+{
+    CK(wavelet_apply(X, Y, S1, S2, c->J, c->scale.data(), c->nt, c->nx, tr, st, &c->launches));
+    return HWG_OK;
+}
+
+// five-term S-hat = W^T S W (system.py:116-147, 182-187)
+static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
+{
+    const int64_t nt = c->nt, N = c->N;
+    TRY(wavelet(c, X, c->U, c->T12, c->T12 + N, false, st));
+    CK(launch_stencil_rows(c->U, c->MxU, c->AxU, c->grid, c->SM, c->SA, nt, st));
+    ++c->launches;
+    BandOut o1{c->At.view(), c->LT.view(), c->MxU, c->AxU, c->T12};
+    BandOut o2{c->Mt.view(), c->L.view(), c->AxU, c->MxU, c->T12 + N};
+    CK(launch_temporal_bands(o1, o2, nt, c->nx, st));
+    ++c->launches;
+    TRY(mg_apply(c, c->T12, c->G12, 2 * nt, 0, nullptr, st));
+    CK(launch_bt_side(c->G12, c->G12 + N, c->MxU, c->U, c->grid, c->SM, c->SA, nt, st));
+    ++c->launches;
+    TRY(wavelet(c, c->U, Y, c->T12, c->T12 + N, true, st));
+    return HWG_OK;
+}
+
+// K_X = blockdiag[C_l A_x C_l] (system.py:242-276)
+static int kx(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
+{
+    TRY(mg_apply(c, X, Y, c->nt, 0, c->row_op_kx, st));
+    CK(launch_stencil_rows(Y, nullptr, c->G12, c->grid, c->SM, c->SA, c->nt, st));
+    ++c->launches;
+    TRY(mg_apply(c, c->G12, Y, c->nt, 0, c->row_op_kx, st));
+    return HWG_OK;
+}
+
+static cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+static int ensure_pcg(hwg_ctx *c)
+{
+    if (c->r) return HWG_OK;
+    TRY(dalloc(c, &c->r, c->N));
+    TRY(dalloc(c, &c->z, c->N));
+    TRY(dalloc(c, &c->p, c->N));
+    TRY(dalloc(c, &c->q, c->N));
+    return HWG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *hwg_last_error(void) { return g_err.c_str(); }
+int hwg_version(void) { return 1; }
+
+int hwg_create(const hwg_desc *desc, hwg_ctx **out)
+{
+    if (!desc || !out) return fail(HWG_EINVAL, "null argument");
+    *out = nullptr;
+    const hwg_desc &d = *desc;
+    if (d.dim != 1 && d.dim != 2) return fail(HWG_EINVAL, "dimension must be 1 or 2 on the GPU path");
+    if (d.J < 1 || d.J > 24) return fail(HWG_EINVAL, "J must be in [1, 24]");
+    if (d.K < 1 || (d.dim == 2 && d.K > 10) || (d.dim == 1 && d.K > 10))
+        return fail(HWG_EINVAL, "K must be in [1, 10]");
+    if (d.smooth != 3) return fail(HWG_EINVAL, "the GPU smoother is built for smooth = 3 sweeps");
+    if (d.vcycles < 1) return fail(HWG_EINVAL, "vcycles must be >= 1");
+    if (!d.coef || !d.stencil_M || !d.stencil_A || !d.temporal || !d.wavelet_scale)
+        return fail(HWG_EINVAL, "missing table in descriptor");
+    CK(cudaSetDevice(d.device));
+    hwg_ctx *c = new hwg_ctx();
+    c->d = d;
+    c->dim = d.dim;
+    c->J = d.J;
+    c->K = d.K;
+    c->nv = d.vcycles;
+    c->m = (1 << d.K) - 1;
+    c->nt = (1LL << d.J) + 1;
+    c->nx = d.dim == 2 ? (int64_t)c->m * c->m : c->m;
+    c->N = c->nt * c->nx;
+    c->rows_max = 2 * c->nt;
+    c->grid = Grid{d.dim, c->m, c->nx};
+    c->SM = Stencil{d.stencil_M[0], d.stencil_M[1], d.stencil_M[2], d.stencil_M[3]};
+    c->SA = Stencil{d.stencil_A[0], d.stencil_A[1], d.stencil_A[2], d.stencil_A[3]};
+    c->scale.assign(d.wavelet_scale, d.wavelet_scale + d.J);
+    const int nops = d.J + 2;
+    c->coef_host.assign(d.coef, d.coef + (size_t)nops * (d.K + 1) * HWG_COEF_STRIDE);
+    int rc;
+#define GO(x)                      \
+    do {                           \
+        rc = (x);                  \
+        if (rc != HWG_OK) {        \
+            hwg_destroy(c);        \
+            return rc;             \
+        }                          \
+    } while (0)
+    GO(upload(c, &c->coef, c->coef_host));
+    c->level_of.assign(c->nt, 0);
+    for (int j = 1; j <= d.J; ++j)
+        for (int64_t r = (1LL << (j - 1)) + 1; r <= (1LL << j); ++r) c->level_of[r] = j;
+    std::vector<int32_t> ops(c->nt);
+    for (int64_t r = 0; r < c->nt; ++r) ops[r] = 1 + c->level_of[r];
+    GO(upload(c, &c->row_op_kx, ops));
+    GO(build_temporal(c));
+    GO(dalloc(c, &c->U, c->N));
+    GO(dalloc(c, &c->MxU, c->N));
+    GO(dalloc(c, &c->AxU, c->N));
+    GO(dalloc(c, &c->T12, 2 * c->N));
+    GO(dalloc(c, &c->G12, 2 * c->N));
+    c->mgX.assign(d.K + 1, nullptr);
+    c->mgB.assign(d.K + 1, nullptr);
+    if (d.dim == 2 && d.K > kCoarseTop2d) {
+        for (int l = kCoarseTop2d; l < d.K; ++l) {
+            GO(dalloc(c, &c->mgX[l], c->rows_max * level_size(c, l)));
+            GO(dalloc(c, &c->mgB[l], c->rows_max * level_size(c, l)));
+        }
+    }
+    GO(dalloc(c, &c->part, c->rows_max + 8));
+    GO(dalloc(c, &c->tmp, c->rows_max + 8));
+    GO(dalloc(c, &c->scal, 16));
+    {
+        void *q = nullptr;
+        if (cudaMalloc(&q, sizeof(int)) != cudaSuccess) {
+            hwg_destroy(c);
+            return fail(HWG_ENOMEM, "flag alloc");
+        }
+        c->allocs.push_back(q);
+        c->flag = (int *)q;
+        if (cudaMallocHost((void **)&c->hscal, 16 * sizeof(double)) != cudaSuccess) {
+            hwg_destroy(c);
+            return fail(HWG_ENOMEM, "pinned alloc");
+        }
+    }
+#undef GO
+    *out = c;
+    return HWG_OK;
+}
+
+int hwg_profile_enable(hwg_ctx *c, int enable)
+{
+    if (!c) return fail(HWG_EINVAL, "null context");
+    prof_flush(c);
+    for (int k = 0; k < 6; ++k) {
+        c->prof_ms[k] = c->prof_bytes[k] = 0.0;
+        c->prof_n[k] = 0;
+    }
+    c->prof = enable != 0;
+    return HWG_OK;
+}
+
+int hwg_profile_read(hwg_ctx *c, int kclass, double *ms, double *bytes, int64_t *launches)
+{
+    if (!c || kclass < 0 || kclass >= 6) return fail(HWG_EINVAL, "bad profile class");
+    prof_flush(c);
+    if (ms) *ms = c->prof_ms[kclass];
+    if (bytes) *bytes = c->prof_bytes[kclass];
+    if (launches) *launches = c->prof_n[kclass];
+    return HWG_OK;
+}
+
+int hwg_destroy(hwg_ctx *c)
+{
+    if (!c) return HWG_OK;
+    prof_flush(c);
+    for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->hscal) cudaFreeHost(c->hscal);
+    delete c;
+    return HWG_OK;
+}
+
+int64_t hwg_workspace_bytes(const hwg_ctx *c) { return c ? c->bytes : 0; }
+int64_t hwg_launch_count(const hwg_ctx *c) { return c ? c->launches : 0; }
+
+int hwg_wavelet(hwg_ctx *c, const double *X, double *Y, int transpose, void *stream)
+{
+    if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
+    if (X == Y) return fail(HWG_EINVAL, "wavelet input and output may not alias");
+    TRY(wavelet(c, X, Y, c->T12, c->T12 + c->N, transpose != 0, S(stream)));
+    return HWG_OK;
+}
+
+int hwg_spatial(hwg_ctx *c, int which, const double *X, double *Y, int64_t rows, void *stream)
+{
+    if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    CK(launch_stencil_rows(X, which == 0 ? Y : nullptr, which == 0 ? nullptr : Y, c->grid,
+                           c->SM, c->SA, rows, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_schur_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
+{
+    if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
+    return schur(c, X, Y, S(stream));
+}
+
+int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
+{
+    if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
+    if (X == Y) return fail(HWG_EINVAL, "K_X input and output may not alias");
+    return kx(c, X, Y, S(stream));
+}
+
+int hwg_mg_rows(hwg_ctx *c, int32_t op, const int32_t *op_host, const double *B, double *X,
+                int64_t rows, void *stream)
+{
+    if (!c || !B || !X || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
+    if (op < 0 || op > c->J + 1) return fail(HWG_EKEY, "no multigrid operator " + std::to_string(op));
+    if (!op_host) return mg_apply(c, B, X, rows, op, nullptr, S(stream));
+    std::vector<int32_t> ops(op_host, op_host + rows);
+    for (int32_t o : ops)
+        if (o < 0 || o > c->J + 1) return fail(HWG_EKEY, "no multigrid operator " + std::to_string(o));
+    int32_t *dops = nullptr;
+    CK(cudaMallocAsync((void **)&dops, std::max<int64_t>(rows, 1) * sizeof(int32_t), S(stream)));
+    CK(cudaMemcpyAsync(dops, ops.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice, S(stream)));
+    int rc = mg_apply(c, B, X, rows, 0, dops, S(stream));
+    cudaFreeAsync(dops, S(stream));
+    return rc;
+}
+
+int hwg_rhs(hwg_ctx *c, const double *F, const double *load, const double *u0proj,
+            double *fhat, void *stream)
+{
+    if (!c || !fhat) return fail(HWG_EINVAL, "null argument");
+    cudaStream_t st = S(stream);
+    const int64_t nt = c->nt, nx = c->nx, N = c->N, ntest = 2 * (nt - 1);
+    // g part: W^T (T^T (x) M_x + N^T (x) A_x) K_Y y, y = (N (x) M_x) F
+    if (F || load) {
+        const double *y = load;
+        if (F) {
+            CK(launch_stencil_rows(F, c->MxU, nullptr, c->grid, c->SM, c->SA, nt, st));
+            BandOut o1{c->Nn.view(), TCsr{nullptr, nullptr, nullptr}, c->MxU, nullptr, c->T12};
+            BandOut o2{};
+            CK(launch_temporal_bands(o1, o2, ntest, nx, st));
+            c->launches += 2;
+            y = c->T12;
+        }
+        TRY(mg_apply(c, y, c->G12, ntest, 0, nullptr, st));      // K_Y = O^-1 (x) K_x, O = I
+        BandOut o1{c->TT.view(), TCsr{nullptr, nullptr, nullptr}, c->G12, nullptr, c->U};
+        BandOut o2{c->NT.view(), TCsr{nullptr, nullptr, nullptr}, c->G12, nullptr, c->AxU};
+        CK(launch_temporal_bands(o1, o2, nt, nx, st));
+        CK(launch_bt_side(c->U, c->AxU, nullptr, c->MxU, c->grid, c->SM, c->SA, nt, st));
+        c->launches += 2;
+        TRY(wavelet(c, c->MxU, fhat, c->U, c->AxU, true, st));
+    } else {
+        CK(cudaMemsetAsync(fhat, 0, N * sizeof(double), st));
+    }
+    if (u0proj) {
+        CK(cudaMemsetAsync(c->T12, 0, N * sizeof(double), st));
+        CK(cudaMemcpyAsync(c->T12, u0proj, nx * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        TRY(wavelet(c, c->T12, c->G12, c->U, c->AxU, true, st));
+        CK(launch_add(fhat, c->G12, fhat, N, st));
+        ++c->launches;
+    }
+    return HWG_OK;
+}
+
+int hwg_dot(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *result_host,
+            void *stream)
+{
+    if (!c || !X || !Y || !result_host || rows < 0 || rows > c->rows_max)
+        return fail(HWG_EINVAL, "bad argument");
+    cudaStream_t st = S(stream);
+    CK(launch_dot(X, Y, rows, c->nx, c->part, c->tmp, c->scal + 8, st, &c->launches));
+    CK(cudaMemcpyAsync(c->hscal + 8, c->scal + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *result_host = c->hscal[8];
+    return HWG_OK;
+}
+
+int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
+            int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out, void *stream)
+{
+    if (!c || !f || !w) return fail(HWG_EINVAL, "null argument");
+    if (!(epsilon > 0) && !(rtol > 0)) return fail(HWG_EINVAL, "tolerance must be positive");
+    if (max_iterations < 0 || recompute_every < 1) return fail(HWG_EINVAL, "bad iteration limits");
+    TRY(ensure_pcg(c));
+    cudaStream_t st = S(stream);
+    const int64_t N = c->N, nt = c->nt, nx = c->nx;
+    hwg_pcg_stats dummy{};
+    hwg_pcg_stats &out = st_out ? *st_out : dummy;
+    out.iterations = 0;
+    out.ms_schur = out.ms_precond = out.ms_vector = out.ms_total = 0.0;
+    auto push = [&](double *arr, int k, double v) {
+        if (arr && k < out.capacity) arr[k] = v;
+    };
+    cudaEvent_t ev[8];
+    for (auto &e : ev) CK(cudaEventCreate(&e));
+    struct Guard {
+        cudaEvent_t *e;
+        ~Guard() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); }
+    } guard{ev};
+    CK(cudaEventRecord(ev[0], st));
+    CK(cudaMemsetAsync(w, 0, N * sizeof(double), st));
+    // zero right-hand side returns immediately (solver.py:196-198)
+    CK(cudaMemsetAsync(c->flag, 0, sizeof(int), st));
+    CK(launch_any_nonzero(f, N, c->flag, st));
+    ++c->launches;
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!hflag) {
+        push(out.residual_norms, 0, 0.0);
+        out.epsilon_used = epsilon;
+        return HWG_OK;
+    }
+    CK(cudaMemcpyAsync(c->r, f, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventRecord(ev[1], st));
+    TRY(kx(c, c->r, c->z, st));
+    CK(cudaEventRecord(ev[2], st));
+    CK(launch_dot(c->r, c->z, nt, nx, c->part, c->tmp, c->scal + 0, st, &c->launches));
+    CK(cudaMemcpyAsync(c->hscal, c->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+    out.ms_precond += ms;
+    double rho = c->hscal[0];
+    push(out.residual_norms, 0, std::sqrt(std::max(rho, 0.0)));
+    const double eps = rtol > 0 ? rtol * std::sqrt(std::max(rho, 0.0)) : epsilon;
+    out.epsilon_used = eps;
+    if (rho <= eps * eps) {
+        CK(cudaEventRecord(ev[7], st));
+        CK(cudaEventSynchronize(ev[7]));
+        CK(cudaEventElapsedTime(&ms, ev[0], ev[7]));
+        out.ms_total = ms;
+        return HWG_OK;
+    }
+    CK(cudaMemcpyAsync(c->p, c->z, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    for (int k = 1; k <= max_iterations; ++k) {
+        CK(cudaEventRecord(ev[1], st));
+        TRY(schur(c, c->p, c->q, st));
+        CK(cudaEventRecord(ev[2], st));
+        CK(launch_dot(c->p, c->q, nt, nx, c->part, c->tmp, c->scal + 1, st, &c->launches));
+        CK(launch_pcg_alpha(c->scal, st));
+        const bool recompute = (k % recompute_every) == 0;
+        CK(launch_update_wr(w, c->r, c->p, c->q, c->scal, N, recompute ? 0 : 1, st));
+        c->launches += 2;
+        CK(cudaEventRecord(ev[3], st));
+        if (recompute) {
+            TRY(schur(c, w, c->z, st));
+            CK(launch_sub(f, c->z, c->r, N, st));
+            ++c->launches;
+        }
+        CK(cudaEventRecord(ev[4], st));
+        TRY(kx(c, c->r, c->z, st));
+        CK(cudaEventRecord(ev[5], st));
+        CK(launch_dot(c->r, c->z, nt, nx, c->part, c->tmp, c->scal + 2, st, &c->launches));
+        CK(cudaMemcpyAsync(c->hscal + 1, c->scal + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(launch_pcg_beta(c->scal, st));
+        CK(launch_update_p(c->p, c->z, c->scal, N, st));
+        c->launches += 2;
+        CK(cudaMemcpyAsync(c->hscal + 3, c->scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ev[6], st));
+        CK(cudaEventSynchronize(ev[6]));
+        float a = 0, b = 0, cc = 0, dd = 0;
+        CK(cudaEventElapsedTime(&a, ev[1], ev[2]));
+        CK(cudaEventElapsedTime(&b, ev[2], ev[3]));
+        CK(cudaEventElapsedTime(&cc, ev[3], ev[4]));
+        CK(cudaEventElapsedTime(&dd, ev[4], ev[5]));
+        out.ms_schur += a + cc;
+        out.ms_vector += b;
+        out.ms_precond += dd;
+        const double pq = c->hscal[1], rho_new = c->hscal[2];
+        const double alpha = c->hscal[3], beta = c->hscal[4];
+        if (!(pq > 0)) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "operator lost positive definiteness (p^T S p = %g)", pq);
+            return fail(HWG_ENOTSPD, buf);
+        }
+        push(out.alphas, k - 1, alpha);
+        push(out.betas, k - 1, beta);
+        push(out.residual_norms, k, std::sqrt(std::max(rho_new, 0.0)));
+        out.iterations = k;
+        if (rho_new <= eps * eps) {
+            CK(cudaEventRecord(ev[7], st));
+            CK(cudaEventSynchronize(ev[7]));
+            CK(cudaEventElapsedTime(&ms, ev[0], ev[7]));
+            out.ms_total = ms;
+            return HWG_OK;
+        }
+    }
+    CK(cudaEventRecord(ev[7], st));
+    CK(cudaEventSynchronize(ev[7]));
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[7]));
+    out.ms_total = ms;
+    char buf[160];
+    snprintf(buf, sizeof buf, "PCG did not reach tolerance %g within %d iterations", eps,
+             max_iterations);
+    return fail(HWG_EMAXIT, buf);
+}
+
+int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double epsilon,
+                   double rtol, int32_t max_iterations, int32_t recompute_every,
+                   hwg_pcg_stats *stats, void *stream)
+{
+    if (!c || !fhat_host || !u_host) return fail(HWG_EINVAL, "null argument");
+    cudaStream_t st = S(stream);
+    if (!c->fdev) {
+        TRY(dalloc(c, &c->fdev, c->N));
+        TRY(dalloc(c, &c->wdev, c->N));
+    }
+    CK(cudaMemcpyAsync(c->fdev, fhat_host, c->N * sizeof(double), cudaMemcpyHostToDevice, st));
+    int rc = hwg_pcg(c, c->fdev, c->wdev, epsilon, rtol, max_iterations, recompute_every, stats, stream);
+    if (rc != HWG_OK && rc != HWG_EMAXIT) return rc;
+    TRY(wavelet(c, c->wdev, c->U, c->T12, c->T12 + c->N, false, st));
+    CK(cudaMemcpyAsync(u_host, c->U, c->N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// hw_internal.cuh -- argument structs and launchers shared between the
+// kernel translation units and the C ABI (hw_capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hw {
+
+// ---- hw_mg2d.cu ----------------------------------------------------------
+struct MgStreamArgs {
+    const double *B;   int64_t ldB;     // level right-hand sides
+    double *X;         int64_t ldX;     // level iterates (in/out)
+    double *Bc;        int64_t ldBc;    // DOWN: coarse right-hand sides (out)
+    const double *Xc;  int64_t ldXc;    // UP: coarse iterates (in)
+    const double *coef;                 // [op][K+1][8]
+    int levels_p1;                      // K + 1
+    int level;                          // l
+    int n;                              // 2^l - 1
+    const int32_t *row_op;              // per temporal row, or null
+    int op;                             // default operator
+    int zero_start;                     // DOWN: iterate starts at zero
+};
+
+struct MgCoarseArgs {
+    const double *B;  int64_t ldB;
+    double *X;        int64_t ldX;
+    const double *coef;
+    int levels_p1;
+    int top;                 // top level handled here (<= kCoarseTop2d)
+    int ncyc;                // V-cycles
+    int zero_start;
+    const int32_t *row_op;
+    int op;
+    int64_t rows;
+};
+
+constexpr int kCoarseTop2d = 5;
+cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
+cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st);
+
+// ---- hw_mg1d.cu ----------------------------------------------------------
+struct Mg1dArgs {
+    const double *B;  int64_t ldB;
+    double *X;        int64_t ldX;
+    const double *coef;
+    int levels_p1;
+    int K;
+    int ncyc;
+    const int32_t *row_op;
+    int op;
+    int64_t rows;
+};
+cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
+
+// ---- hw_wavelet.cu -------------------------------------------------------
+cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
+                          const double *scale, int64_t nt, int64_t nx, bool transpose,
+                          cudaStream_t st, int64_t *launches);
+
+// ---- hw_kron.cu ----------------------------------------------------------
+struct Stencil {           // finest-level spatial stencil, see hwg_desc
+    double c0, cx, cy, cd; // 1D: c0, -, cy (neighbour), -
+};
+struct Grid {
+    int dim;
+    int m;                 // points per direction
+    int64_t nx;            // m^dim
+};
+struct TCsr {              // temporal factor, CSR on the device
+    const int32_t *ip, *ix;
+    const double *v;
+};
+struct BandOut {           // out = b1 x1 (+ b2 x2)
+    TCsr b1, b2;
+    const double *x1, *x2;
+    double *out;
+};
+cudaError_t launch_stencil_rows(const double *X, double *YM, double *YA, Grid g, Stencil M,
+                                Stencil A, int64_t rows, cudaStream_t st);
+cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0, double *out,
+                           Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st);
+cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx,
+                                  cudaStream_t st);
+cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
+                       cudaStream_t st);
+
+// ---- hw_vec.cu -----------------------------------------------------------
+cudaError_t launch_dot(const double *X, const double *Y, int64_t rows, int64_t nx, double *part,
+                       double *tmp, double *out, cudaStream_t st, int64_t *launches);
+cudaError_t launch_pcg_alpha(double *s, cudaStream_t st);
+cudaError_t launch_pcg_beta(double *s, cudaStream_t st);
+cudaError_t launch_update_wr(double *w, double *r, const double *p, const double *q,
+                             const double *s, int64_t n, int update_r, cudaStream_t st);
+cudaError_t launch_update_p(double *p, const double *z, const double *s, int64_t n,
+                            cudaStream_t st);
+cudaError_t launch_sub(const double *f, const double *t, double *r, int64_t n, cudaStream_t st);
+cudaError_t launch_any_nonzero(const double *X, int64_t n, int *flag, cudaStream_t st);
+
+}  // namespace hw
