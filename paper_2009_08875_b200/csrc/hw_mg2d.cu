@@ -28,263 +28,332 @@
 #include "hw_common.cuh"
 #include "hw_internal.cuh"
 
+#include <type_traits>
+
 namespace hw {
 
 // ring sizes, see the lifetime analysis in DESIGN.md §MG
-template <bool DOWN> struct Rings;
-template <> struct Rings<true> { static constexpr int RX = 11, RB = 9, RR = 4, RC = 0; };
-template <> struct Rings<false> { static constexpr int RX = 10, RB = 7, RR = 0, RC = 4; };
+// ---------------------------------------------------------------------------
+// streamed fine-level passes
+// ---------------------------------------------------------------------------
+// Ring slots: row i of a ring lives in slot (i mod R), R a power of two.  The
+// step loop is unrolled by 4 so every slot offset is a compile-time constant
+// (the 8-slot b ring needs one uniform select per block of 4 steps).
+// Lifetimes (steps; row i is swept by sweep s at step i + 2(s-1), b is
+// prefetched one step ahead):  V0 i-2..i (DOWN) / i-3..i (UP),  V1 i..i+2,
+// V2 i+2..i+4,  V3 i+4..i+7,  b i-1..i+6,  residual i+6..i+7.
+struct RingsDown { static constexpr int V0 = 4, V1 = 4, V2 = 4, V3 = 4, B = 8, R = 2, C = 0; };
+struct RingsUp { static constexpr int V0 = 4, V1 = 4, V2 = 4, V3 = 4, B = 8, R = 0, C = 4; };
+template <bool DOWN> using RingsOf = typename std::conditional<DOWN, RingsDown, RingsUp>::type;
+constexpr int kMaxWarpCarry = 4;       // warp totals summed for a chunk carry
 
-template <int PPT, int NT, bool DOWN>
+template <int P, int NT, bool DOWN>
 __host__ __device__ constexpr size_t stream_smem_words(int n)
 {
-    // x ring (padded n+2), b ring (n), r ring (n), coarse ring (m+2),
-    // zero row (n+2), scan scratch (NW*3 + powers)
-    return (size_t)Rings<DOWN>::RX * (n + 2) + (size_t)Rings<DOWN>::RB * n +
-           (size_t)Rings<DOWN>::RR * n + (size_t)Rings<DOWN>::RC * ((n - 1) / 2 + 2) +
-           (size_t)(n + 2) + 3 * (NT / 32) + 3 * 40;
+    using G = RingsOf<DOWN>;
+    const size_t W = (size_t)n + 2;
+    const size_t Wc = (size_t)(n - 1) / 2 + 2;
+    return W * (G::V0 + G::V1 + G::V2 + G::V3 + G::B + G::R + 1) + Wc * G::C +
+           3 * (size_t)(NT / 32 + kMaxWarpCarry) + (P + 1) + 33 + (kMaxWarpCarry + 1) + 8;
 }
 
-template <int PPT, int NT, bool DOWN>
+// Row recurrence.  Thread t owns P consecutive points of a grid row; y_k is
+// the sweep recurrence x_j = p_j + beta x_{j-1} run over the chunk from a
+// zero carry-in and S_t = y_{P-1}.  Within a warp the chunk carries are an
+// exact inclusive scan of S with multiplier gamma = beta^P.  Across warps
+// the carry into warp w is sum_{k>=1} Gamma^(k-1) T_{w-k} (T = warp totals,
+// Gamma = gamma^32 = beta^(32P)); |beta| <= 1/4 for the 2D operators
+// alpha A + mu M, so Gamma <= 2^-(64P) and the nearest warp already leaves a
+// tail below 2^-70 relative -- 2^17 times smaller than one fp64 rounding:
+// the lexicographic Gauss-Seidel result up to rounding.  (Kw, the number of
+// warp totals summed, is computed per CTA and is at most kMaxWarpCarry.)
+template <int P, int NT, bool DOWN>
 __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
 {
-    using R = Rings<DOWN>;
-    constexpr int RRm = R::RR > 0 ? R::RR : 1;   // modulus guards for the
-    constexpr int RCm = R::RC > 0 ? R::RC : 1;   // rings a pass does not use
+    using G = RingsOf<DOWN>;
     constexpr int NW = NT / 32;
-    constexpr int D = 2;
-    extern __shared__ double sm[];
+    constexpr int KW = kMaxWarpCarry;
+    constexpr int MJ = (NT * P / 2 + NT - 1) / NT;      // coarse columns per thread (DOWN)
+    extern __shared__ __align__(16) double sm[];
 
     const int n = a.n;
-    const int W = n + 2;
+    const int W = n + 2;                                // data at 1..n, zero pads at 0, n+1
     const int m = (n - 1) / 2;
+    const int Wc = m + 2;
     const int64_t row = blockIdx.x;
     const int op = a.row_op ? a.row_op[row] : a.op;
     const double *cf = a.coef + ((int64_t)op * a.levels_p1 + a.level) * kCoefStride;
     const double c0 = cf[kC0], cx = cf[kCx], cy = cf[kCy], cd = cf[kCd], inv = cf[kInv];
     const double beta = -cy * inv;
 
-    double *xs = sm;                                   // RX * W
-    double *bs = xs + R::RX * W;                       // RB * n
-    double *rs = bs + R::RB * n;                       // RR * n
-    double *cs = rs + R::RR * n;                       // RC * (m+2)
-    double *zr = cs + R::RC * (m + 2);                 // W zeros
-    double *wt = zr + W;                               // NW * 3 warp totals
-    double *gp = wt + 3 * NW;                          // powers: gamma^l (33), beta^k (PPT+1)
+    double *const v0 = sm;
+    double *const v1 = v0 + G::V0 * W;
+    double *const v2 = v1 + G::V1 * W;
+    double *const v3 = v2 + G::V2 * W;
+    double *const bs = v3 + G::V3 * W;
+    double *const rs = bs + G::B * W;
+    double *const zr = rs + G::R * W;                   // a row of zeros
+    double *const cs = zr + W;                          // coarse ring (UP)
+    double *const sc = cs + G::C * Wc;                  // warp totals [3][KW + NW]
+    double *const gp = sc + 3 * (NW + KW);              // beta^0..P, gamma^0..32, Gamma^0..KW
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int j0 = tid * P;                             // first local column of this thread
+    const int nvalid = n - j0 < 0 ? 0 : (n - j0 > P ? P : n - j0);
+    const int jb = nvalid > 0 ? j0 : 0;                 // idle threads compute on row data
     const double *Bg = a.B + row * a.ldB;
     double *Xg = a.X + row * a.ldX;
 
-    // powers of beta and gamma = beta^PPT (uniform per CTA)
+    const double ab = fabs(beta);
+    int Kw = 0;
+    if (ab > 0.0) {
+        Kw = ab >= 0.9 ? KW : (int)ceil(70.0 / (32.0 * P * -log2(ab)));
+        Kw = Kw > KW ? KW : (Kw < 1 ? 1 : Kw);
+    }
     if (tid == 0) {
         double bp = 1.0;
-        for (int k = 0; k <= PPT; ++k) { gp[33 + k] = bp; bp *= beta; }
-        const double g = gp[33 + PPT];
+        for (int k = 0; k <= P; ++k) { gp[k] = bp; bp *= beta; }
+        const double g = gp[P];
         double q = 1.0;
-        for (int l = 0; l <= 32; ++l) { gp[l] = q; q *= g; }
+        for (int k = 0; k <= 32; ++k) { gp[P + 1 + k] = q; q *= g; }
+        const double Gm = gp[P + 1 + 32];
+        q = 1.0;
+        for (int k = 0; k <= KW; ++k) { gp[P + 34 + k] = k < Kw ? q : 0.0; q *= Gm; }
     }
-    for (int k = tid; k < W; k += NT) zr[k] = 0.0;
-    for (int s = 0; s < R::RX; ++s)
-        for (int k = tid; k < W; k += NT) xs[s * W + k] = 0.0;
-    if (!DOWN)
-        for (int s = 0; s < R::RC; ++s)
-            for (int k = tid; k < m + 2; k += NT) cs[s * (m + 2) + k] = 0.0;
+    {
+        const int total = (int)(gp - sm);
+        for (int k = tid; k < total; k += NT) sm[k] = 0.0;
+    }
     __syncthreads();
+    const double gl = gp[P + 1 + lane];                 // gamma^lane
+    double Gw[KW];                                      // Gamma^(k) weights (0 beyond Kw)
+#pragma unroll
+    for (int k = 0; k < KW; ++k) Gw[k] = gp[P + 34 + k];
+    double bpow[P];                                     // beta^(k+1)
+#pragma unroll
+    for (int k = 0; k < P; ++k) bpow[k] = gp[k + 1];
+    double gscan[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) gscan[k] = gp[P + 1 + (1 << k)];
 
-    auto xrow = [&](int i) -> double * { return (i < 0 || i >= n) ? zr : xs + (i % R::RX) * W; };
-    auto brow = [&](int i) -> double * { return bs + (i % R::RB) * n; };
-    auto crow = [&](int c) -> const double * {
-        return (c < 0 || c >= m) ? zr : cs + (c % RCm) * (m + 2);
+    constexpr int gs = DOWN ? 1 : -1;                   // UP runs point-reversed
+    auto grow = [&](const double *base, int i) -> const double * {
+        return base + (DOWN ? (int64_t)i * n : (int64_t)(n - 1 - i) * n + (n - 1));
     };
-    // global index of (grid row i, col j) in the pass's own (possibly
-    // reversed) coordinates
-    auto gidx = [&](int i, int j) -> int64_t {
-        return DOWN ? (int64_t)i * n + j : (int64_t)(n - 1 - i) * n + (n - 1 - j);
-    };
+    const bool zs = DOWN && a.zero_start;
 
-    // issue the loads of "virtual step" s: b row s+D; x row s+D+1 (DOWN,
-    // unless zero start) or s+D+2 (UP) and the coarse row it first needs.
+    // loads of virtual step s: b row s+1; raw x row s+2 (DOWN) / s+3 (UP)
+    // plus, UP, the coarse row it first needs.  Rows >= n get zeros.
     auto issue = [&](int s) {
-        const int ib = s + D;
+        const int ib = s + 1;
         if (ib >= 0 && ib < n) {
-            double *dst = brow(ib);
-            for (int j = tid; j < n; j += NT) cp_async8(dst + j, Bg + gidx(ib, j));
+            double *dst = bs + (ib & (G::B - 1)) * W + 1;
+            const double *src = grow(Bg, ib);
+            for (int e = tid; e < n; e += NT) cp_async8(dst + e, src + gs * e);
         }
-        const int ix = DOWN ? s + D + 1 : s + D + 2;
-        if (ix >= 0 && ix < n) {
-            double *dst = xs + (ix % R::RX) * W + 1;
-            if (DOWN && a.zero_start) {
-                for (int j = tid; j < n; j += NT) dst[j] = 0.0;
+        const int ix = DOWN ? s + 2 : s + 3;
+        if (ix >= 0 && !zs) {
+            double *dst = v0 + (ix & (G::V0 - 1)) * W + 1;
+            if (ix < n) {
+                const double *src = grow(Xg, ix);
+                for (int e = tid; e < n; e += NT) cp_async8(dst + e, src + gs * e);
             } else {
-                for (int j = tid; j < n; j += NT) cp_async8(dst + j, Xg + gidx(ix, j));
+                for (int e = tid; e < n; e += NT) dst[e] = 0.0;
             }
-            if (!DOWN && (ix % 2 == 0) && ix / 2 < m) {
-                // coarse row c = ix/2 (reversed coordinates) first used by fine row 2c
-                const int c = ix / 2;
-                const double *Xc = a.Xc + row * a.ldXc;
-                double *cdst = cs + (c % RCm) * (m + 2) + 1;
-                for (int J = tid; J < m; J += NT)
-                    cp_async8(cdst + J, Xc + (int64_t)(m - 1 - c) * m + (m - 1 - J));
-            }
+        }
+        if (!DOWN && ix >= 0 && ix < n && !(ix & 1) && ix / 2 < m) {
+            const int c = ix / 2;                       // coarse row first used by fine row 2c
+            const double *Xc = a.Xc + row * a.ldXc;
+            double *cdst = cs + (c & (G::C - 1)) * Wc + 1;
+            for (int e = tid; e < m; e += NT)
+                cp_async8(cdst + e, Xc + (int64_t)(m - 1 - c) * m + (m - 1 - e));
         }
         cp_async_commit();
     };
 
-    // x[i] += P x_coarse (reversed coordinates, spatial.py:140-173)
+    // UP: V0[i] += P x_coarse (local = point-reversed coordinates)
     auto prolongate = [&](int i) {
         if (i < 0 || i >= n) return;
-        double *xr = xs + (i % R::RX) * W + 1;
-        const double *ca, *cb;
-        if (i & 1) { ca = crow((i - 1) / 2); cb = nullptr; }
-        else { ca = crow(i / 2 - 1); cb = crow(i / 2); }
+        double *xr = v0 + (i & (G::V0 - 1)) * W + 1;
+        auto crow = [&](int c) -> const double * {
+            return (c < 0 || c >= m) ? zr : cs + (c & (G::C > 0 ? G::C - 1 : 0)) * Wc;
+        };
+        const double *ca = (i & 1) ? crow((i - 1) / 2) : crow(i / 2 - 1);
+        const double *cb = (i & 1) ? ca : crow(i / 2);
         for (int j = tid; j < n; j += NT) {
             double v;
-            if (i & 1) {
-                if (j & 1) v = ca[1 + (j - 1) / 2];
-                else v = 0.5 * ca[1 + j / 2 - 1] + 0.5 * ca[1 + j / 2];
+            if (j & 1) {
+                const int J = (j - 1) / 2 + 1;
+                v = (i & 1) ? ca[J] : 0.5 * ca[J] + 0.5 * cb[J];
             } else {
-                if (j & 1) v = 0.5 * ca[1 + (j - 1) / 2] + 0.5 * cb[1 + (j - 1) / 2];
-                else v = 0.5 * ca[1 + j / 2 - 1] + 0.5 * cb[1 + j / 2];
+                const int J = j / 2;                    // padded index of coarse j/2 - 1
+                v = (i & 1) ? 0.5 * ca[J] + 0.5 * ca[J + 1] : 0.5 * ca[J] + 0.5 * cb[J + 1];
             }
             xr[j] += v;
         }
     };
 
-    // prologue
-    const int first = DOWN ? -D - 1 : -D - 2;
-    for (int s = first; s < 0; ++s) issue(s);
+    for (int s = DOWN ? -2 : -3; s < 0; ++s) issue(s);
     if (!DOWN) {
-        cp_async_wait<D>();
+        cp_async_wait<1>();
         __syncthreads();
         prolongate(0);
         prolongate(1);
     }
 
-    const int j0 = tid * PPT;
+    // coarse right-hand-side accumulator (DOWN): coarse row I collects the
+    // restricted residual rows 2I (top), 2I+1 (centre), 2I+2 (bottom)
+    // (R = P^T, spatial.py:140-173)
+    double acc[MJ];
+#pragma unroll
+    for (int k = 0; k < MJ; ++k) acc[k] = 0.0;
+
     const int nsteps = DOWN ? n + 7 : n + 4;
+    for (int t0 = 0; t0 < nsteps; t0 += 4) {
+        const int h8 = (t0 >> 2) & 1;                   // b ring half for this block
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u;
+            if (t >= nsteps) break;
+            cp_async_wait<0>();
+            __syncthreads();                            // (#0) loads + last step's rows visible
+            issue(t);
 
-    for (int t = 0; t < nsteps; ++t) {
-        cp_async_wait<D - 1>();
-        __syncthreads();
-        issue(t);
+            // slot of row t - k in a ring of size R (compile-time for R <= 4)
+#define SLOT(base, R, k) ((base) + (((u - (k)) & ((R) - 1))) * W)
+#define BSLOT(k) (bs + ((((h8 << 2) + u - (k)) & 7)) * W)
 
-        // ---------------- phase A: right-hand sides from old values ----------
-        double p[3][PPT];
-        bool act[3];
-#pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            const int i = t - 2 * s;
-            act[s] = (i >= 0 && i < n);
-            if (!act[s]) {
-#pragma unroll
-                for (int k = 0; k < PPT; ++k) p[s][k] = 0.0;
-                continue;
-            }
-            const double *xu = xrow(i - 1) + 1, *xc = xrow(i) + 1, *xd = xrow(i + 1) + 1;
-            const double *br = brow(i);
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-                const int j = j0 + k;
-                double acc = 0.0;
-                if (j < n) {
-                    acc = br[j];
-                    acc -= cd * xu[j - 1];
-                    acc -= cx * xu[j];
-                    acc -= cy * xc[j + 1];
-                    acc -= cx * xd[j];
-                    acc -= cd * xd[j + 1];
-                    acc *= inv;
-                }
-                p[s][k] = acc;
-            }
-        }
-        if (DOWN) {
-            const int ir = t - 6;
-            if (ir >= 0 && ir < n) {
-                const double *xu = xrow(ir - 1) + 1, *xc = xrow(ir) + 1, *xd = xrow(ir + 1) + 1;
-                const double *br = brow(ir);
-                double *rr = rs + (ir % RRm) * n;
-                for (int j = tid; j < n; j += NT) {
-                    double acc = br[j];
-                    acc -= cd * xu[j - 1];
-                    acc -= cx * xu[j];
-                    acc -= cy * xc[j - 1];
-                    acc -= c0 * xc[j];
-                    acc -= cy * xc[j + 1];
-                    acc -= cx * xd[j];
-                    acc -= cd * xd[j + 1];
-                    rr[j] = acc;
-                }
-            }
-            if ((t & 1) && t >= 9) {
-                const int I = (t - 9) / 2;
-                if (I < m) {
-                    const double *r0 = rs + ((2 * I) % RRm) * n;
-                    const double *r1 = rs + ((2 * I + 1) % RRm) * n;
-                    const double *r2 = rs + ((2 * I + 2) % RRm) * n;
-                    double *bc = a.Bc + row * a.ldBc + (int64_t)I * m;
-                    for (int J = tid; J < m; J += NT) {
-                        const int c = 2 * J;
-                        double acc = 0.5 * r0[c];
-                        acc += 0.5 * r0[c + 1];
-                        acc += 0.5 * r1[c];
-                        acc += r1[c + 1];
-                        acc += 0.5 * r1[c + 2];
-                        acc += 0.5 * r2[c + 1];
-                        acc += 0.5 * r2[c + 2];
-                        bc[J] = acc;
-                    }
-                }
-            }
-        }
-        __syncthreads();
-
-        // ---------------- phase B: affine scans along the rows ---------------
-        double S[3];
-#pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            double y = 0.0;
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) { y = fma(beta, y, p[s][k]); p[s][k] = y; }
-            S[s] = y;
-        }
-        // inclusive warp scan of T_l = S_l + gamma T_{l-1}
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double g = gp[o];
+            // ---- phase A: p_j = (b - known neighbours)/c0 and chunk recurrence ----
+            double p[3][P];
+            double S[3];
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
-                const double v = __shfl_up_sync(0xffffffffu, S[s], o);
-                if (lane >= o) S[s] = fma(g, v, S[s]);
+                const double *up, *cur, *dn;
+                if (s == 0) {
+                    up = SLOT(v1, G::V1, 1);
+                    cur = zs ? zr : SLOT(v0, G::V0, 0);
+                    dn = zs ? zr : SLOT(v0, G::V0, -1);
+                } else if (s == 1) {
+                    up = SLOT(v2, G::V2, 3);
+                    cur = SLOT(v1, G::V1, 2);
+                    dn = SLOT(v1, G::V1, 1);
+                } else {
+                    up = SLOT(v3, G::V3, 5);
+                    cur = SLOT(v2, G::V2, 4);
+                    dn = SLOT(v2, G::V2, 3);
+                }
+                const double *bb = BSLOT(2 * s) + 1 + jb;
+                up += jb;
+                cur += jb;
+                dn += jb;
+                double uu[P + 1], dd[P + 1], cc[P];
+#pragma unroll
+                for (int k = 0; k <= P; ++k) { uu[k] = up[k]; dd[k] = dn[k + 1]; }
+#pragma unroll
+                for (int k = 0; k < P; ++k) cc[k] = cur[k + 2];
+                double y = 0.0;
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    const double e1 = fma(-cd, uu[k], bb[k]);
+                    const double e2 = uu[k + 1] + dd[k];
+                    const double e3 = fma(cd, dd[k + 1], cy * cc[k]);
+                    y = fma(beta, y, (fma(-cx, e2, e1) - e3) * inv);
+                    p[s][k] = y;
+                }
+                S[s] = y;
             }
-        }
-        if (lane == 31)
+            // restriction (DOWN): residual row t-7 (written last step) into
+            // the coarse accumulators; coarse row I completes with fine row 2I+2
+            if (DOWN) {
+                const int r = t - 7;
+                if (r >= 0 && r < n) {
+                    const double *rr = rs + (r & 1) * W;
+                    double *bc = a.Bc + row * a.ldBc + (int64_t)(r / 2 - 1) * m;
 #pragma unroll
-            for (int s = 0; s < 3; ++s) wt[warp * 3 + s] = S[s];
-        __syncthreads();
-        const double G32 = gp[32];
-#pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            double Cw = 0.0;
-            for (int v = 0; v < warp; ++v) Cw = fma(G32, Cw, wt[v * 3 + s]);
-            const double prev = __shfl_up_sync(0xffffffffu, S[s], 1);
-            const double carry = (lane == 0) ? Cw : fma(gp[lane], Cw, prev);
-            if (act[s]) {
-                const int i = t - 2 * s;
-                double *xr = xs + (i % R::RX) * W + 1;
-#pragma unroll
-                for (int k = 0; k < PPT; ++k) {
-                    const int j = j0 + k;
-                    if (j < n) {
-                        const double v = fma(gp[33 + k + 1], carry, p[s][k]);
-                        xr[j] = v;
-                        if (s == 2) Xg[gidx(i, j)] = v;
+                    for (int k = 0; k < MJ; ++k) {
+                        const int J = tid + k * NT;
+                        if (J < m) {
+                            const int c = 2 * J;
+                            if (r & 1) {          // centre row of coarse (r-1)/2
+                                acc[k] += fma(0.5, rr[c] + rr[c + 2], rr[c + 1]);
+                            } else {              // bottom of coarse r/2-1, top of r/2
+                                if (r >= 2) bc[J] = acc[k] + 0.5 * (rr[c + 1] + rr[c + 2]);
+                                acc[k] = 0.5 * (rr[c] + rr[c + 1]);
+                            }
+                        }
                     }
                 }
             }
+
+            // ---- exact warp scan of chunk ends T_l = S_l + gamma T_{l-1} ----
+#pragma unroll
+            for (int o = 1, q = 0; o < 32; o <<= 1, ++q) {
+#pragma unroll
+                for (int s = 0; s < 3; ++s) {
+                    const double v = __shfl_up_sync(0xffffffffu, S[s], o);
+                    if (lane >= o) S[s] = fma(gscan[q], v, S[s]);
+                }
+            }
+            if (lane == 31) {
+#pragma unroll
+                for (int s = 0; s < 3; ++s) sc[s * (NW + KW) + KW + warp] = S[s];
+            }
+            __syncthreads();                            // (#1) warp totals visible
+
+            // ---- phase B: carries, write the swept rows ----
+            double *const Xrow = const_cast<double *>(grow(Xg, t - 4));
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const int i = t - 2 * s;
+                const double *sp = sc + s * (NW + KW) + KW + warp;
+                double Cw = 0.0;
+#pragma unroll
+                for (int k = 0; k < KW; ++k) Cw = fma(Gw[k], sp[-1 - k], Cw);
+                const double prev = __shfl_up_sync(0xffffffffu, S[s], 1);
+                const double carry = (lane == 0) ? Cw : fma(gl, Cw, prev);
+                if (i < 0 || i > n) continue;           // row n is written as zeros
+                double *xr = (s == 0 ? SLOT(v1, G::V1, 0)
+                                     : (s == 1 ? SLOT(v2, G::V2, 2) : SLOT(v3, G::V3, 4))) + 1 + j0;
+                if (i == n) {
+#pragma unroll
+                    for (int k = 0; k < P; ++k) if (k < nvalid) xr[k] = 0.0;
+                    continue;
+                }
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    if (k < nvalid) {
+                        const double v = fma(bpow[k], carry, p[s][k]);
+                        xr[k] = v;
+                        if (s == 2) Xrow[gs * (j0 + k)] = v;
+                    }
+                }
+            }
+
+            if (DOWN) {
+                // residual of grid row t-6 (final iterate rows t-7..t-5)
+                const int ir = t - 6;
+                if (ir >= 0 && ir < n) {
+                    const double *up = SLOT(v3, G::V3, 7) + jb;
+                    const double *cur = SLOT(v3, G::V3, 6) + jb;
+                    const double *dn = SLOT(v3, G::V3, 5) + jb;
+                    const double *bb = BSLOT(6) + 1 + jb;
+                    double *rr = rs + (ir & 1) * W + jb;
+#pragma unroll
+                    for (int k = 0; k < P; ++k) {
+                        const double e1 = fma(-cd, up[k], bb[k]);
+                        const double e2 = up[k + 1] + dn[k + 1];
+                        const double e3 = cur[k] + cur[k + 2];
+                        const double e4 = fma(cd, dn[k + 2], c0 * cur[k + 1]);
+                        const double acc = fma(-cy, e3, fma(-cx, e2, e1)) - e4;
+                        if (k < nvalid) rr[k] = acc;
+                    }
+                }
+            } else {
+                prolongate(t + 2);
+            }
+#undef SLOT
+#undef BSLOT
         }
-        if (!DOWN) prolongate(t + 2);
     }
     cp_async_wait<0>();
 }
@@ -438,18 +507,20 @@ static cudaError_t launch_stream_t(const MgStreamArgs &a, int64_t rows, cudaStre
 
 cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
-    // NT * PPT >= n; one CTA per temporal row
+    // one CTA per temporal row; P (odd) consecutive points per thread so a
+    // warp's 64-bit shared loads at stride 8P bytes are bank-conflict free
+    // (P = 5 measured faster than P = 3 with 11 warps at n = 1023)
     const int n = a.n;
-    if (n <= 64)
-        return down ? launch_stream_t<2, 32, true>(a, rows, st) : launch_stream_t<2, 32, false>(a, rows, st);
-    if (n <= 128)
-        return down ? launch_stream_t<4, 32, true>(a, rows, st) : launch_stream_t<4, 32, false>(a, rows, st);
-    if (n <= 256)
-        return down ? launch_stream_t<4, 64, true>(a, rows, st) : launch_stream_t<4, 64, false>(a, rows, st);
-    if (n <= 512)
-        return down ? launch_stream_t<4, 128, true>(a, rows, st) : launch_stream_t<4, 128, false>(a, rows, st);
-    if (n <= 1024)
-        return down ? launch_stream_t<4, 256, true>(a, rows, st) : launch_stream_t<4, 256, false>(a, rows, st);
+    if (n <= 96)
+        return down ? launch_stream_t<3, 32, true>(a, rows, st) : launch_stream_t<3, 32, false>(a, rows, st);
+    if (n <= 160)
+        return down ? launch_stream_t<5, 32, true>(a, rows, st) : launch_stream_t<5, 32, false>(a, rows, st);
+    if (n <= 320)
+        return down ? launch_stream_t<5, 64, true>(a, rows, st) : launch_stream_t<5, 64, false>(a, rows, st);
+    if (n <= 640)
+        return down ? launch_stream_t<5, 128, true>(a, rows, st) : launch_stream_t<5, 128, false>(a, rows, st);
+    if (n <= 1120)
+        return down ? launch_stream_t<5, 224, true>(a, rows, st) : launch_stream_t<5, 224, false>(a, rows, st);
     return cudaErrorInvalidValue;
 }
 
