@@ -278,7 +278,9 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get(dname)
+            rec = json.load(fh).get(dname)
+        if rec:   # measured dram bytes / algorithmic bytes, scaled to this run's launches
+            traffic = rec["traffic_over_algorithmic"] * dbytes / max(dn, 1)
     model = model_bytes_per_iteration(d, J, K)
     it_s = (ms_max / 1e3) / total_its
 
@@ -352,9 +354,9 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=(1, 2, 3, 4))
+    ap.add_argument("--config", type=int, default=4, choices=(1, 2, 3, 4))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-iterations", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")

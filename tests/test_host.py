@@ -1,0 +1,134 @@
+"""CPU-only checks: the C ABI library, host setup, inputs, bench helpers."""
+import ctypes
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+from paper_2009_08875_b200 import _lib, discretization as disc, inputs
+from paper_2009_08875_b200 import api
+
+
+def _header_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        names |= set(re.findall(r"\b(hwg_[a-z_]+)\s*\(", src))
+    return names
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2009_08875_b200 import build
+    build.build()
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    syms = _header_symbols()
+    assert len(syms) >= 15
+    for name in sorted(syms):
+        assert hasattr(lib, name), name
+    assert set(_lib.EXPORTS) == syms
+    L = _lib.load()
+    assert L.hwg_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "d1"])
+def test_stencils_bit_identical_to_reference(name):
+    meta, _ = golden(name)
+    d = meta["d"]
+    for lvl, st in enumerate(meta["stencils"], start=1):
+        M, A = disc.level_stencils(d, lvl)
+        m = 2 ** lvl - 1
+        keymap = {0: "c0", 1: "cy"} if d == 1 else {0: "c0", 1: "cy", m: "cx", m + 1: "cd"}
+        for ours, offs, vals in ((A, st["A_off"], st["A"]), (M, st["M_off"], st["M"])):
+            ref = {keymap[o]: v for o, v in zip(offs, vals) if o >= 0 and o in keymap}
+            for k, v in ref.items():
+                assert ours[k] == v, (name, lvl, k)
+            for k, v in ours.items():
+                assert ref.get(k, 0.0) == v, (name, lvl, k)
+
+
+def test_coef_table_matches_scipy_sum():
+    import scipy.sparse as sp
+    from oracle import heatwave_oracle as O
+    d, J, K, alpha = 2, 3, 4, 0.3
+    tab = disc.coef_table(d, J, K, alpha)
+    levels = [O.mesh(d, k) for k in range(1, K + 1)]
+    for l, lv in enumerate(levels, start=1):
+        M, A = O.assemble_p1(lv)
+        for o, (a, mu) in enumerate(disc.operator_list(J, alpha)):
+            S = (a * A + mu * M).tocsr()
+            r = S.shape[0] // 2
+            row = dict(zip((S[r].indices - r).tolist(), S[r].data.tolist()))
+            m = 2 ** l - 1
+            assert tab[o, l, 0] == row[0]
+            if l >= 2:
+                assert tab[o, l, 2] == row.get(1, 0.0)
+                assert tab[o, l, 1] == row.get(m, 0.0)
+                assert tab[o, l, 3] == row.get(m + 1, 0.0)
+
+
+def test_temporal_values_and_levels():
+    t = disc.temporal_values(3)
+    h = 1 / 8
+    assert t[0] == h / 6 and t[1] == 2 * h / 3 and t[4] == 2.0 / h
+    assert np.array_equal(disc.level_of(3), [0, 0, 1, 2, 2, 3, 3, 3, 3])
+    assert disc.wavelet_scales(2)[1] == 2.0
+
+
+def test_project_initial_matches_golden():
+    for name in ("c1", "d1"):
+        meta, g = golden(name)
+        mesh = disc.FineMesh(meta["d"], meta["K"])
+        u0 = inputs.u0_sines if meta["dist"] == "uniform" else inputs.u0_modes()
+        assert np.array_equal(disc.project_initial(mesh, u0), g["u0proj"])
+
+
+def test_forcing_is_split_invariant():
+    full = inputs.forcing("uniform", 200, 7)
+    parts = np.concatenate([inputs.forcing_rows("uniform", 200, 7, a, b)
+                            for a, b in ((0, 37), (37, 130), (130, 200))])
+    assert np.array_equal(full, parts)
+    assert inputs.forcing("normal", 5, 3).shape == (5, 3)
+
+
+def test_host_api_helpers():
+    v = np.random.default_rng(0).standard_normal(129)
+    assert abs(api.tree_reduce(v) - v.sum()) < 1e-12
+    assert api.split_ranges(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    plan = api.ParallelPlan.create(3, 10)
+    plan.validate()
+    with pytest.raises(ValueError):
+        api.ParallelPlan(2, ((0, 4), (5, 10)), 1).validate()
+    d, e = api.lanczos_tridiagonal([1.0, 0.5], [0.25, 0.1])
+    assert d[0] == 1.0 and d[1] == 2.0 + 0.25
+
+
+def test_problem_data_validation():
+    with pytest.raises(ValueError):
+        disc.ProblemData(D=np.array([[1.0, 2.0], [0.0, 1.0]]), c=0.0, u0=lambda x: x[:, 0])
+    with pytest.raises(ValueError):
+        disc.ProblemData(D=np.eye(2), c=-1.0, u0=lambda x: x[:, 0])
+
+
+def test_bench_model_bytes_match_survey():
+    import bench
+    per = {1: 2149.6, 2: 2261.6, 3: 3319.0, 4: 2267.4}
+    for cfg, want in per.items():
+        d, J, K, *_ = inputs.recipe(cfg)
+        N = (2 ** J + 1) * (2 ** K - 1) ** d
+        assert abs(bench.model_bytes_per_iteration(d, J, K) / N - want) < 0.05
+
+
+def test_no_oracle_import_in_product():
+    for path in glob.glob(os.path.join(ROOT, "paper_2009_08875_b200", "**", "*.py"), recursive=True):
+        src = open(path).read()
+        assert "oracle" not in src.replace("oracle/", ""), path
