@@ -351,11 +351,10 @@ static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
 {
     const int64_t nt = c->nt, N = c->N;
     TRY(wavelet(c, X, c->U, c->T12, c->T12 + N, false, st));
-    CK(launch_stencil_rows(c->U, c->MxU, c->AxU, c->grid, c->SM, c->SA, nt, st));
-    ++c->launches;
-    BandOut o1{c->At.view(), c->LT.view(), c->MxU, c->AxU, c->T12};
-    BandOut o2{c->Mt.view(), c->L.view(), c->AxU, c->MxU, c->T12 + N};
-    CK(launch_temporal_bands(o1, o2, nt, c->nx, st));
+    // t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU (one pass over U); the
+    // first row of MxU is kept for the trace term
+    CK(launch_bside_fused(c->U, c->T12, c->T12 + N, c->MxU, c->grid, c->SM, c->SA, c->At.view(),
+                          c->LT.view(), c->Mt.view(), c->L.view(), nt, st));
     ++c->launches;
     TRY(mg_apply(c, c->T12, c->G12, 2 * nt, 0, nullptr, st));
     CK(launch_bt_side(c->G12, c->G12 + N, c->MxU, c->U, c->grid, c->SM, c->SA, nt, st));

@@ -82,6 +82,9 @@ cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0,
                            Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st);
 cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx,
                                   cudaStream_t st);
+cudaError_t launch_bside_fused(const double *U, double *T1, double *T2, double *E0, Grid g,
+                               Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
+                               int64_t nt, cudaStream_t st);
 cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
                        cudaStream_t st);
 

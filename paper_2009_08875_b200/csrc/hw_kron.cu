@@ -3,81 +3,172 @@
 // Spatial factors are the finest-level P1 stencils (spatial.py:202-229) on
 // the lexicographic interior grid; temporal factors are the tridiagonal
 // trial matrices M_t, A_t, L (temporal.py:82-115) and the test matrices
-// T, N (temporal.py:118-144).  Every value is accumulated in the
+// T, N (temporal.py:118-144) in CSR form.  Every value is accumulated in the
 // reference's CSR column order without FMA contraction (csr_rows_matvec
 // _kernels.py:25-34, temporal_apply :37-52), so these kernels reproduce the
 // reference bit for bit.
+//
+// Geometry: a CTA of 64 x 4 threads covers 64 consecutive y-points (j) of 4
+// grid rows (i) of one temporal row (2D), or 256 points (1D); temporal rows
+// run over blockIdx.z with a grid-stride loop.  No integer division per
+// element.  Neighbour reads go through the read-only cache (a tile's halo is
+// reused by its 7-point stencils).
 #include "hw_common.cuh"
 #include "hw_internal.cuh"
 
 namespace hw {
 
+constexpr int TX = 64, TY = 4;
 
+struct Pt {          // a grid point of one temporal row
+    int i, j;        // 2D: (x index, y index); 1D: (0, index)
+    bool ok;
+};
 
-// y = S x at flattened interior index k of one row (CSR column order); the
-// diagonal coupling exists in the CSR only where its value is nonzero
-__device__ __forceinline__ double stencil_at(const double *__restrict__ x, int64_t k,
+__device__ __forceinline__ Pt point_of(const Grid &g)
+{
+    Pt p;
+    if (g.dim == 2) {
+        p.j = blockIdx.x * TX + threadIdx.x;
+        p.i = blockIdx.y * TY + threadIdx.y;
+        p.ok = p.i < g.m && p.j < g.m;
+    } else {
+        p.i = 0;
+        p.j = (blockIdx.x * TY + threadIdx.y) * TX + threadIdx.x;
+        p.ok = p.j < g.m;
+    }
+    return p;
+}
+
+// y = S x at one point (CSR column order; the diagonal coupling exists in
+// the CSR only where its value is nonzero)
+__device__ __forceinline__ double stencil_pt(const double *__restrict__ x, const Pt &p,
                                              const Grid &g, const Stencil &s)
 {
+    const int m = g.m;
     if (g.dim == 1) {
-        const int i = (int)k;
-        double acc = 0.0;
-        bool first = true;
-        auto add = [&](double v) { acc = first ? v : add_rn(acc, v); first = false; };
-        if (i > 0) add(mul_rn(s.cy, x[k - 1]));
-        add(mul_rn(s.c0, x[k]));
-        if (i < g.m - 1) add(mul_rn(s.cy, x[k + 1]));
+        const int j = p.j;
+        double acc = mul_rn(s.c0, __ldg(x + j));
+        if (j > 0) acc = add_rn(mul_rn(s.cy, __ldg(x + j - 1)), acc);
+        if (j < m - 1) acc = add_rn(acc, mul_rn(s.cy, __ldg(x + j + 1)));
         return acc;
     }
-    const int m = g.m;
-    const bool HAS_DIAG = s.cd != 0.0;
-    const int i = (int)(k / m), j = (int)(k - (int64_t)i * m);
+    const bool diag = s.cd != 0.0;
+    const int i = p.i, j = p.j;
+    const int64_t k = (int64_t)i * m + j;
     double acc = 0.0;
     bool first = true;
     auto add = [&](double v) { acc = first ? v : add_rn(acc, v); first = false; };
-    if (HAS_DIAG && i > 0 && j > 0) add(mul_rn(s.cd, x[k - m - 1]));
-    if (i > 0) add(mul_rn(s.cx, x[k - m]));
-    if (j > 0) add(mul_rn(s.cy, x[k - 1]));
-    add(mul_rn(s.c0, x[k]));
-    if (j < m - 1) add(mul_rn(s.cy, x[k + 1]));
-    if (i < m - 1) add(mul_rn(s.cx, x[k + m]));
-    if (HAS_DIAG && i < m - 1 && j < m - 1) add(mul_rn(s.cd, x[k + m + 1]));
+    if (diag && i > 0 && j > 0) add(mul_rn(s.cd, __ldg(x + k - m - 1)));
+    if (i > 0) add(mul_rn(s.cx, __ldg(x + k - m)));
+    if (j > 0) add(mul_rn(s.cy, __ldg(x + k - 1)));
+    add(mul_rn(s.c0, __ldg(x + k)));
+    if (j < m - 1) add(mul_rn(s.cy, __ldg(x + k + 1)));
+    if (i < m - 1) add(mul_rn(s.cx, __ldg(x + k + m)));
+    if (diag && i < m - 1 && j < m - 1) add(mul_rn(s.cd, __ldg(x + k + m + 1)));
     return acc;
 }
 
-// Y1 = M X, Y2 = A X (either output may be null)
-__global__ void stencil_rows(const double *__restrict__ X, double *__restrict__ YM,
-                             double *__restrict__ YA, Grid g, Stencil M, Stencil A, int64_t rows)
+__device__ __forceinline__ int64_t pidx(const Pt &p, const Grid &g)
 {
-    const int64_t total = rows * g.nx;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / g.nx, k = e - r * g.nx;
+    return g.dim == 2 ? (int64_t)p.i * g.m + p.j : p.j;
+}
+
+static dim3 spatial_grid(const Grid &g, int64_t rows)
+{
+    const unsigned z = (unsigned)(rows < 65535 ? (rows < 1 ? 1 : rows) : 65535);
+    if (g.dim == 2) return dim3((g.m + TX - 1) / TX, (g.m + TY - 1) / TY, z);
+    return dim3((g.m + TX * TY - 1) / (TX * TY), 1, z);
+}
+
+// YM = M X, YA = A X (either output may be null)
+__global__ void __launch_bounds__(TX * TY) stencil_rows(const double *__restrict__ X,
+                                                        double *__restrict__ YM,
+                                                        double *__restrict__ YA, Grid g,
+                                                        Stencil M, Stencil A, int64_t rows)
+{
+    const Pt p = point_of(g);
+    if (!p.ok) return;
+    const int64_t k = pidx(p, g);
+    for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) {
         const double *x = X + r * g.nx;
-        if (YM) YM[e] = stencil_at(x, k, g, M);
-        if (YA) YA[e] = stencil_at(x, k, g, A);
+        if (YM) YM[r * g.nx + k] = stencil_pt(x, p, g, M);
+        if (YA) YA[r * g.nx + k] = stencil_pt(x, p, g, A);
     }
 }
 
 // out = M G1 + A G2; row 0 additionally += E0 (the trace term Gamma0 (x) M_x)
 // -- system.py:134,141-142,145
-__global__ void bt_side(const double *__restrict__ G1, const double *__restrict__ G2,
-                        const double *__restrict__ E0, double *__restrict__ out, Grid g,
-                        Stencil M, Stencil A, int64_t rows)
+__global__ void __launch_bounds__(TX * TY) bt_side(const double *__restrict__ G1,
+                                                   const double *__restrict__ G2,
+                                                   const double *__restrict__ E0,
+                                                   double *__restrict__ out, Grid g, Stencil M,
+                                                   Stencil A, int64_t rows)
 {
-    const int64_t total = rows * g.nx;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / g.nx, k = e - r * g.nx;
-        double v = add_rn(stencil_at(G1 + r * g.nx, k, g, M),
-                          stencil_at(G2 + r * g.nx, k, g, A));
+    const Pt p = point_of(g);
+    if (!p.ok) return;
+    const int64_t k = pidx(p, g);
+    for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) {
+        double v = add_rn(stencil_pt(G1 + r * g.nx, p, g, M), stencil_pt(G2 + r * g.nx, p, g, A));
         if (r == 0 && E0) v = add_rn(v, E0[k]);
-        out[e] = v;
+        out[r * g.nx + k] = v;
     }
 }
 
-// Temporal factor in CSR form (device arrays, <= 4 nnz per row).
+// one CSR row of a temporal factor applied to the values of rows c-1, c, c+1
+// (these factors have no other entries)
+__device__ __forceinline__ double band3(const TCsr &B, int64_t c, double vm, double v0, double vp)
+{
+    const int k0 = B.ip[c], k1 = B.ip[c + 1];
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k) {
+        const int d = B.ix[k] - (int)c;
+        const double x = d < 0 ? vm : (d == 0 ? v0 : vp);
+        acc = (k == k0) ? mul_rn(B.v[k], x) : add_rn(acc, mul_rn(B.v[k], x));
+    }
+    return acc;
+}
 
+// B-side, fused: t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU with
+// MxU = M_x U, AxU = A_x U computed on the fly (system.py:119-139).  Each CTA
+// owns a spatial tile and a chunk of temporal rows and slides a 3-row window
+// of (MxU, AxU) in registers, so U is read once and t1, t1' written once.
+// E0 (optional) receives M_x U[0] for the trace term.
+__global__ void __launch_bounds__(TX * TY) bside_fused(const double *__restrict__ U,
+                                                       double *__restrict__ T1,
+                                                       double *__restrict__ T2,
+                                                       double *__restrict__ E0, Grid g,
+                                                       Stencil M, Stencil A, TCsr At, TCsr LT,
+                                                       TCsr Mt, TCsr Lm, int64_t nt, int chunk)
+{
+    const Pt p = point_of(g);
+    if (!p.ok) return;
+    const int64_t k = pidx(p, g);
+    for (int64_t c0 = (int64_t)blockIdx.z * chunk; c0 < nt; c0 += (int64_t)gridDim.z * chunk) {
+        const int64_t c1 = c0 + chunk < nt ? c0 + chunk : nt;
+        double mm = 0.0, am = 0.0;                     // row c-1
+        if (c0 > 0) {
+            mm = stencil_pt(U + (c0 - 1) * g.nx, p, g, M);
+            am = stencil_pt(U + (c0 - 1) * g.nx, p, g, A);
+        }
+        double m0 = stencil_pt(U + c0 * g.nx, p, g, M);
+        double a0 = stencil_pt(U + c0 * g.nx, p, g, A);
+        if (c0 == 0 && E0) E0[k] = m0;
+        for (int64_t c = c0; c < c1; ++c) {
+            double mp = 0.0, ap = 0.0;                 // row c+1
+            if (c + 1 < nt) {
+                mp = stencil_pt(U + (c + 1) * g.nx, p, g, M);
+                ap = stencil_pt(U + (c + 1) * g.nx, p, g, A);
+            }
+            T1[c * g.nx + k] = add_rn(band3(At, c, mm, m0, mp), band3(LT, c, am, a0, ap));
+            T2[c * g.nx + k] = add_rn(band3(Mt, c, am, a0, ap), band3(Lm, c, mm, m0, mp));
+            mm = m0; am = a0;
+            m0 = mp; a0 = ap;
+        }
+    }
+}
+
+// O1 = B1 X1 (+ B2 X2), O2 likewise; any B may be absent (ip null)
 __device__ __forceinline__ double tcsr_row(const TCsr &B, int64_t c, const double *__restrict__ X,
                                            int64_t i, int64_t nx)
 {
@@ -88,24 +179,18 @@ __device__ __forceinline__ double tcsr_row(const TCsr &B, int64_t c, const doubl
     return acc;
 }
 
-// O1 = B1 X1 (+ B2 X2), O2 = B3 X3 (+ B4 X4); any B may be "absent" (ip null)
-// -- t1 = A_t MxU + L^T AxU and t1' = M_t AxU + L MxU (system.py:130-139)
-
 __global__ void temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx)
 {
-    const int64_t total = rows * nx;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = e / nx, i = e - c * nx;
-        {
-            double v = tcsr_row(o1.b1, c, o1.x1, i, nx);
-            if (o1.b2.ip) v = add_rn(v, tcsr_row(o1.b2, c, o1.x2, i, nx));
-            o1.out[e] = v;
-        }
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    for (int64_t c = blockIdx.y; c < rows; c += gridDim.y) {
+        double v = tcsr_row(o1.b1, c, o1.x1, i, nx);
+        if (o1.b2.ip) v = add_rn(v, tcsr_row(o1.b2, c, o1.x2, i, nx));
+        o1.out[c * nx + i] = v;
         if (o2.out) {
-            double v = tcsr_row(o2.b1, c, o2.x1, i, nx);
-            if (o2.b2.ip) v = add_rn(v, tcsr_row(o2.b2, c, o2.x2, i, nx));
-            o2.out[e] = v;
+            double w = tcsr_row(o2.b1, c, o2.x1, i, nx);
+            if (o2.b2.ip) w = add_rn(w, tcsr_row(o2.b2, c, o2.x2, i, nx));
+            o2.out[c * nx + i] = w;
         }
     }
 }
@@ -129,21 +214,39 @@ static unsigned grid_for(int64_t total, int bs)
 cudaError_t launch_stencil_rows(const double *X, double *YM, double *YA, Grid g, Stencil M,
                                 Stencil A, int64_t rows, cudaStream_t st)
 {
-    stencil_rows<<<grid_for(rows * g.nx, 256), 256, 0, st>>>(X, YM, YA, g, M, A, rows);
+    stencil_rows<<<spatial_grid(g, rows), dim3(TX, TY), 0, st>>>(X, YM, YA, g, M, A, rows);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0, double *out,
                            Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st)
 {
-    bt_side<<<grid_for(rows * g.nx, 256), 256, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
+    bt_side<<<spatial_grid(g, rows), dim3(TX, TY), 0, st>>>(G1, G2, E0, out, g, M, A, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bside_fused(const double *U, double *T1, double *T2, double *E0, Grid g,
+                               Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
+                               int64_t nt, cudaStream_t st)
+{
+    // temporal chunks: enough CTAs for ~8 per SM, at least 8 rows per chunk
+    dim3 grid = spatial_grid(g, 1);
+    const int64_t tiles = (int64_t)grid.x * grid.y;
+    int64_t chunks = (148LL * 8 + tiles - 1) / tiles;
+    int chunk = (int)((nt + chunks - 1) / chunks);
+    if (chunk < 8) chunk = 8;
+    chunks = (nt + chunk - 1) / chunk;
+    grid.z = (unsigned)(chunks < 65535 ? chunks : 65535);
+    bside_fused<<<grid, dim3(TX, TY), 0, st>>>(U, T1, T2, E0, g, M, A, At, LT, Mt, L, nt, chunk);
     return cudaGetLastError();
 }
 
 cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx,
                                   cudaStream_t st)
 {
-    temporal_bands<<<grid_for(rows * nx, 256), 256, 0, st>>>(o1, o2, rows, nx);
+    dim3 grid((unsigned)((nx + 255) / 256),
+              (unsigned)(rows < 65535 ? (rows < 1 ? 1 : rows) : 65535));
+    temporal_bands<<<grid, 256, 0, st>>>(o1, o2, rows, nx);
     return cudaGetLastError();
 }
 

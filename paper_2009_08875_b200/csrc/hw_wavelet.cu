@@ -24,16 +24,14 @@ namespace hw {
 __device__ __forceinline__ double qa(double s, int k) { return s * (k == 0 ? -1.0 : -0.5); }
 __device__ __forceinline__ double qb(double s, int k, int nw) { return s * (k == nw - 1 ? -1.0 : -0.5); }
 
-// dst rows [0, nf) <- M_j [c ; d]
+// dst rows [0, nf) <- M_j [c ; d]; grid: (column blocks, stage rows)
 __global__ void wav_syn_stage(const double *__restrict__ C, const double *__restrict__ Dm,
                               double *__restrict__ Y, int j, double s, int64_t nx)
 {
     const int nc = (1 << (j - 1)) + 1, nf = (1 << j) + 1, nw = 1 << (j - 1);
-    const int64_t total = (int64_t)nf * nx;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(e / nx);
-        const int64_t i = e - (int64_t)r * nx;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    for (int r = blockIdx.y; r < nf; r += gridDim.y) {
         double acc;
         if ((r & 1) == 0) {
             const int q = r >> 1;                 // coarse index
@@ -48,7 +46,7 @@ __global__ void wav_syn_stage(const double *__restrict__ C, const double *__rest
             acc = add_rn(acc, mul_rn(0.5, C[(int64_t)(k + 1) * nx + i]));
             acc = add_rn(acc, mul_rn(s, Dm[(int64_t)(nc + k) * nx + i]));
         }
-        Y[e] = acc;
+        Y[(int64_t)r * nx + i] = acc;
     }
 }
 
@@ -57,11 +55,9 @@ __global__ void wav_ana_stage(const double *__restrict__ X, double *__restrict__
                               double *__restrict__ Dout, int j, double s, int64_t nx)
 {
     const int nc = (1 << (j - 1)) + 1, nf = (1 << j) + 1, nw = 1 << (j - 1);
-    const int64_t total = (int64_t)nf * nx;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(e / nx);
-        const int64_t i = e - (int64_t)r * nx;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    for (int r = blockIdx.y; r < nf; r += gridDim.y) {
         if (r < nc) {
             // column r of P_j: rows 2r-1 (1/2), 2r (1), 2r+1 (1/2)
             double acc;
@@ -83,11 +79,9 @@ __global__ void wav_ana_stage(const double *__restrict__ X, double *__restrict__
     }
 }
 
-static unsigned grid_for(int64_t total, int bs)
+static dim3 stage_grid(int64_t rows, int64_t nx, int bs)
 {
-    int64_t g = (total + bs - 1) / bs;
-    const int64_t cap = 148LL * 16;
-    return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+    return dim3((unsigned)((nx + bs - 1) / bs), (unsigned)(rows < 65535 ? rows : 65535));
 }
 
 // Y = W X (transpose = 0) or W^T X (transpose = 1).  S1 (and S2 for the
@@ -105,8 +99,8 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         const double *src = X;
         for (int j = 1; j <= J; ++j) {
             double *dst = ((J - j) % 2 == 0) ? Y : S1;
-            const int64_t total = ((1LL << j) + 1) * nx;
-            wav_syn_stage<<<grid_for(total, bs), bs, 0, st>>>(src, X, dst, j, scale[j - 1], nx);
+            wav_syn_stage<<<stage_grid((1LL << j) + 1, nx, bs), bs, 0, st>>>(src, X, dst, j,
+                                                                          scale[j - 1], nx);
             ++*launches;
             src = dst;
         }
@@ -114,8 +108,8 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         const double *src = X;
         for (int j = J; j >= 1; --j) {
             double *cdst = (j == 1) ? Y : (((J - j) % 2 == 0) ? S1 : S2);
-            const int64_t total = ((1LL << j) + 1) * nx;
-            wav_ana_stage<<<grid_for(total, bs), bs, 0, st>>>(src, cdst, Y, j, scale[j - 1], nx);
+            wav_ana_stage<<<stage_grid((1LL << j) + 1, nx, bs), bs, 0, st>>>(src, cdst, Y, j,
+                                                                          scale[j - 1], nx);
             ++*launches;
             src = cdst;
         }
