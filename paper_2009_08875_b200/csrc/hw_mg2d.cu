@@ -361,14 +361,141 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
 // ---------------------------------------------------------------------------
 // coarse levels in shared memory, one warp per temporal row
 // ---------------------------------------------------------------------------
-constexpr int kCoarseWords = 2 * (1 + 9 + 49 + 225 + 961) + 961;  // x, b, r
+// Level L (m = 2^L - 1 points per direction) is stored with row pitch 2^L so
+// the anti-diagonal wavefront stride (pitch - 1 = m, odd) keeps a warp's
+// 64-bit shared accesses bank-conflict free.
+template <int L>
+struct Lc {
+    static constexpr int m = (1 << L) - 1;
+    static constexpr int pitch = 1 << L;
+    static constexpr int size = pitch * m;
+    static constexpr int off = Lc<L - 1>::off + Lc<L - 1>::size;
+};
+template <>
+struct Lc<0> { static constexpr int m = 0, pitch = 1, size = 0, off = 0; };
+constexpr int kCoarseStack = Lc<kCoarseTop2d>::off + Lc<kCoarseTop2d>::size;
+constexpr int kCoarseWords = 2 * kCoarseStack + Lc<kCoarseTop2d>::size;   // x, b, r
 
-__device__ __forceinline__ int lvl_off(int l)
+// one point update in CSR column order (the reference's arithmetic)
+template <int L>
+__device__ __forceinline__ void gs_point(double *x, const double *b, const double *c, int i, int j)
 {
-    // offset of level l (1-based) in the concatenated hierarchy
-    int o = 0;
-    for (int k = 1; k < l; ++k) o += ((1 << k) - 1) * ((1 << k) - 1);
-    return o;
+    constexpr int m = Lc<L>::m, p = Lc<L>::pitch;
+    const int k = i * p + j;
+    double acc = b[k];
+    if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[k - p - 1]);
+    if (i > 0) acc = sub_mul(acc, c[kCx], x[k - p]);
+    if (j > 0) acc = sub_mul(acc, c[kCy], x[k - 1]);
+    if (j < m - 1) acc = sub_mul(acc, c[kCy], x[k + 1]);
+    if (i < m - 1) acc = sub_mul(acc, c[kCx], x[k + p]);
+    if (i < m - 1 && j < m - 1 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[k + p + 1]);
+    x[k] = __ddiv_rn(acc, c[kC0]);
+}
+
+// lexicographic GS (forward) or its reverse by anti-diagonal wavefronts
+template <int L>
+__device__ __forceinline__ void coarse_sweep(double *xw, const double *bw, const double *c,
+                                             bool forward, int lane)
+{
+    constexpr int m = Lc<L>::m;
+    double *x = xw + Lc<L>::off;
+    const double *b = bw + Lc<L>::off;
+    for (int dd = 0; dd <= 2 * m - 2; ++dd) {
+        const int d = forward ? dd : 2 * m - 2 - dd;
+        const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
+        const int ihi = d < m - 1 ? d : m - 1;
+        for (int i = ilo + lane; i <= ihi; i += 32) gs_point<L>(x, b, c, i, d - i);
+        __syncwarp();
+    }
+}
+
+template <int L>
+__device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw,
+                                              const double *coef, int lane)
+{
+    if constexpr (L >= 2) {
+        constexpr int m = Lc<L>::m, p = Lc<L>::pitch, mc = Lc<L - 1>::m, pc = Lc<L - 1>::pitch;
+        const double *c = coef + L * kCoefStride;
+        for (int s = 0; s < 3; ++s) coarse_sweep<L>(xw, bw, c, true, lane);
+        double *x = xw + Lc<L>::off;
+        const double *b = bw + Lc<L>::off;
+        for (int k = lane; k < m * m; k += 32) {           // residual
+            const int i = k / m, j = k % m, q = i * p + j;
+            double acc = b[q];
+            if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[q - p - 1]);
+            if (i > 0) acc = sub_mul(acc, c[kCx], x[q - p]);
+            if (j > 0) acc = sub_mul(acc, c[kCy], x[q - 1]);
+            acc = sub_mul(acc, c[kC0], x[q]);
+            if (j < m - 1) acc = sub_mul(acc, c[kCy], x[q + 1]);
+            if (i < m - 1) acc = sub_mul(acc, c[kCx], x[q + p]);
+            if (i < m - 1 && j < m - 1 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[q + p + 1]);
+            rw[q] = acc;
+        }
+        __syncwarp();
+        double *xc = xw + Lc<L - 1>::off, *bc = bw + Lc<L - 1>::off;
+        for (int k = lane; k < mc * mc; k += 32) {         // restrict, R = P^T in CSR order
+            const int I = k / mc, J = k % mc;
+            const double *r0 = rw + (2 * I) * p + 2 * J;
+            const double *r1 = r0 + p, *r2 = r1 + p;
+            double acc = 0.0;
+            acc = add_mul(acc, 0.5, r0[0]);
+            acc = add_mul(acc, 0.5, r0[1]);
+            acc = add_mul(acc, 0.5, r1[0]);
+            acc = add_mul(acc, 1.0, r1[1]);
+            acc = add_mul(acc, 0.5, r1[2]);
+            acc = add_mul(acc, 0.5, r2[1]);
+            acc = add_mul(acc, 0.5, r2[2]);
+            bc[I * pc + J] = acc;
+            xc[I * pc + J] = 0.0;
+        }
+        __syncwarp();
+        coarse_vcycle<L - 1>(xw, bw, rw, coef, lane);
+        const double *xcc = xw + Lc<L - 1>::off;
+        for (int k = lane; k < m * m; k += 32) {           // prolongate (spatial.py:140-173)
+            const int gi = k / m + 1, gj = k % m + 1;      // 1-based fine grid coords
+            auto cv = [&](int I, int J) -> double {        // 1-based coarse coords
+                return (I < 1 || J < 1 || I > mc || J > mc) ? 0.0 : xcc[(I - 1) * pc + (J - 1)];
+            };
+            double acc = 0.0;
+            const int pi = gi & 1, pj = gj & 1;
+            if (!pi && !pj) {
+                acc = add_mul(acc, 1.0, cv(gi / 2, gj / 2));
+            } else {
+                const int ai = (gi - pi) / 2, aj = (gj - pj) / 2;
+                const int bi = (gi + pi) / 2, bj = (gj + pj) / 2;
+                // CSR order: ascending coarse index (a precedes b)
+                if (!(ai < 1 || aj < 1 || ai > mc || aj > mc)) acc = add_mul(acc, 0.5, cv(ai, aj));
+                if (!(bi < 1 || bj < 1 || bi > mc || bj > mc)) acc = add_mul(acc, 0.5, cv(bi, bj));
+            }
+            const int q = (gi - 1) * p + (gj - 1);
+            x[q] = add_rn(x[q], acc);
+        }
+        __syncwarp();
+        for (int s = 0; s < 3; ++s) coarse_sweep<L>(xw, bw, c, false, lane);
+    } else {
+        if (lane == 0) xw[0] = add_mul(0.0, coef[1 * kCoefStride + kCoarse], bw[0]);  // 1x1 solve
+        __syncwarp();
+    }
+}
+
+template <int TOP, int WPB>
+__device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, int64_t row, int lane)
+{
+    constexpr int m = Lc<TOP>::m, p = Lc<TOP>::pitch;
+    double *bw = xw + kCoarseStack;
+    double *rw = bw + kCoarseStack;
+    const int op = a.row_op ? a.row_op[row] : a.op;
+    const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
+    const double *Bg = a.B + row * a.ldB;
+    double *Xg = a.X + row * a.ldX;
+    for (int k = lane; k < m * m; k += 32) {
+        const int q = Lc<TOP>::off + (k / m) * p + k % m;
+        bw[q] = Bg[k];
+        xw[q] = a.zero_start ? 0.0 : Xg[k];
+    }
+    __syncwarp();
+    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP>(xw, bw, rw, coef, lane);
+    for (int k = lane; k < m * m; k += 32) Xg[k] = xw[Lc<TOP>::off + (k / m) * p + k % m];
 }
 
 template <int WPB>
@@ -379,116 +506,13 @@ __global__ void __launch_bounds__(32 * WPB) mg2d_coarse(MgCoarseArgs a)
     const int64_t row = (int64_t)blockIdx.x * WPB + w;
     if (row >= a.rows) return;
     double *xw = sm + (size_t)w * kCoarseWords;
-    double *bw = xw + (kCoarseWords - 961) / 2;
-    double *rw = bw + (kCoarseWords - 961) / 2;
-    const int op = a.row_op ? a.row_op[row] : a.op;
-    const int top = a.top;
-    const int mt = (1 << top) - 1;
-    const int ot = lvl_off(top);
-    const double *Bg = a.B + row * a.ldB;
-    double *Xg = a.X + row * a.ldX;
-    for (int k = lane; k < mt * mt; k += 32) {
-        bw[ot + k] = Bg[k];
-        xw[ot + k] = a.zero_start ? 0.0 : Xg[k];
+    switch (a.top) {
+    case 1: coarse_row<1, WPB>(a, xw, row, lane); break;
+    case 2: coarse_row<2, WPB>(a, xw, row, lane); break;
+    case 3: coarse_row<3, WPB>(a, xw, row, lane); break;
+    case 4: coarse_row<4, WPB>(a, xw, row, lane); break;
+    default: coarse_row<5, WPB>(a, xw, row, lane); break;
     }
-    __syncwarp();
-
-    auto C = [&](int l) { return a.coef + ((int64_t)op * a.levels_p1 + l) * kCoefStride; };
-
-    // one point update in CSR column order (the reference's arithmetic)
-    auto gs_point = [&](double *x, const double *b, const double *c, int m, int i, int j) {
-        double acc = b[i * m + j];
-        if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[(i - 1) * m + j - 1]);
-        if (i > 0) acc = sub_mul(acc, c[kCx], x[(i - 1) * m + j]);
-        if (j > 0) acc = sub_mul(acc, c[kCy], x[i * m + j - 1]);
-        if (j < m - 1) acc = sub_mul(acc, c[kCy], x[i * m + j + 1]);
-        if (i < m - 1) acc = sub_mul(acc, c[kCx], x[(i + 1) * m + j]);
-        if (i < m - 1 && j < m - 1 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[(i + 1) * m + j + 1]);
-        x[i * m + j] = __ddiv_rn(acc, c[kC0]);
-    };
-    auto sweep = [&](int l, bool forward) {
-        const int m = (1 << l) - 1;
-        double *x = xw + lvl_off(l);
-        const double *b = bw + lvl_off(l);
-        const double *c = C(l);
-        for (int dd = 0; dd <= 2 * m - 2; ++dd) {
-            const int d = forward ? dd : 2 * m - 2 - dd;
-            const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
-            const int ihi = d < m - 1 ? d : m - 1;
-            for (int i = ilo + lane; i <= ihi; i += 32) gs_point(x, b, c, m, i, d - i);
-            __syncwarp();
-        }
-    };
-
-    for (int cyc = 0; cyc < a.ncyc; ++cyc) {
-        for (int l = top; l >= 2; --l) {
-            const int m = (1 << l) - 1, mc = (1 << (l - 1)) - 1;
-            for (int s = 0; s < 3; ++s) sweep(l, true);
-            double *x = xw + lvl_off(l);
-            const double *b = bw + lvl_off(l);
-            const double *c = C(l);
-            for (int k = lane; k < m * m; k += 32) {      // residual
-                const int i = k / m, j = k % m;
-                double acc = b[k];
-                if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[k - m - 1]);
-                if (i > 0) acc = sub_mul(acc, c[kCx], x[k - m]);
-                if (j > 0) acc = sub_mul(acc, c[kCy], x[k - 1]);
-                acc = sub_mul(acc, c[kC0], x[k]);
-                if (j < m - 1) acc = sub_mul(acc, c[kCy], x[k + 1]);
-                if (i < m - 1) acc = sub_mul(acc, c[kCx], x[k + m]);
-                if (i < m - 1 && j < m - 1 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[k + m + 1]);
-                rw[k] = acc;
-            }
-            __syncwarp();
-            double *xc = xw + lvl_off(l - 1), *bc = bw + lvl_off(l - 1);
-            for (int k = lane; k < mc * mc; k += 32) {    // restrict
-                const int I = k / mc, J = k % mc;
-                const double *r0 = rw + (2 * I) * m + 2 * J;
-                const double *r1 = r0 + m, *r2 = r1 + m;
-                double acc = 0.0;
-                acc = add_mul(acc, 0.5, r0[0]);
-                acc = add_mul(acc, 0.5, r0[1]);
-                acc = add_mul(acc, 0.5, r1[0]);
-                acc = add_mul(acc, 1.0, r1[1]);
-                acc = add_mul(acc, 0.5, r1[2]);
-                acc = add_mul(acc, 0.5, r2[1]);
-                acc = add_mul(acc, 0.5, r2[2]);
-                bc[k] = acc;
-                xc[k] = 0.0;
-            }
-            __syncwarp();
-        }
-        if (lane == 0) xw[0] = add_mul(0.0, C(1)[kCoarse], bw[0]);  // 1x1 coarse solve
-        __syncwarp();
-        for (int l = 2; l <= top; ++l) {
-            const int m = (1 << l) - 1, mc = (1 << (l - 1)) - 1;
-            double *x = xw + lvl_off(l);
-            const double *xc = xw + lvl_off(l - 1);
-            for (int k = lane; k < m * m; k += 32) {       // prolongate
-                const int gi = k / m + 1, gj = k % m + 1; // 1-based fine grid coords
-                double acc = 0.0;
-                auto cv = [&](int I, int J) -> double {   // 1-based coarse coords
-                    return (I < 1 || J < 1 || I > mc || J > mc) ? 0.0 : xc[(I - 1) * mc + (J - 1)];
-                };
-                const int pi = gi & 1, pj = gj & 1;
-                if (!pi && !pj) {
-                    acc = add_mul(acc, 1.0, cv(gi / 2, gj / 2));
-                } else {
-                    const int ai = (gi - pi) / 2, aj = (gj - pj) / 2;
-                    const int bi = (gi + pi) / 2, bj = (gj + pj) / 2;
-                    const bool aok = !(ai < 1 || aj < 1 || ai > mc || aj > mc);
-                    const bool bok = !(bi < 1 || bj < 1 || bi > mc || bj > mc);
-                    // CSR order: ascending coarse index (a precedes b)
-                    if (aok) acc = add_mul(acc, 0.5, cv(ai, aj));
-                    if (bok) acc = add_mul(acc, 0.5, cv(bi, bj));
-                }
-                x[k] = add_rn(x[k], acc);
-            }
-            __syncwarp();
-            for (int s = 0; s < 3; ++s) sweep(l, false);
-        }
-    }
-    for (int k = lane; k < mt * mt; k += 32) Xg[k] = xw[ot + k];
 }
 
 // ---------------------------------------------------------------------------
