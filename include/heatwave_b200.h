@@ -77,6 +77,12 @@ typedef struct {
     const double *stencil_A;
     const double *temporal;
     const double *wavelet_scale;
+    /* 0: full context (operator workspaces for all N_t rows).  > 0: kernel
+     * context for the distributed (time-slab) path -- multigrid and dot
+     * workspaces for batches of up to rows_max rows, no N-sized operator
+     * buffers (hwg_schur_apply, hwg_kx_apply, hwg_rhs, hwg_wavelet, hwg_pcg
+     * and hwg_solve_host then return HWG_EINVAL). */
+    int64_t rows_max;
 } hwg_desc;
 
 typedef struct hwg_ctx hwg_ctx;
@@ -179,6 +185,55 @@ int64_t hwg_launch_count(const hwg_ctx *ctx);
  */
 int hwg_profile_enable(hwg_ctx *ctx, int enable);
 int hwg_profile_read(hwg_ctx *ctx, int kclass, double *ms, double *bytes, int64_t *launches);
+
+/* ------------------------------------------------------------------------
+ * Time-slab building blocks (multi-GPU path).  The reference
+ * distributes temporal rows over workers (ParallelPlan, solver.py:47-108)
+ * with halo reads; these entry points compute one rank's share of an
+ * operator given explicitly supplied halo rows.  Rows are named by their
+ * GLOBAL temporal index; `x0`-style arguments give the global index of the
+ * first row an array holds.
+ * ------------------------------------------------------------------------ */
+
+/* Synthesis stage j (wavelet.py:114-137 with M_j of :56-76): Y[f - f0] for
+ * fine nodes f in [f0, f0 + nf) from coarse nodal rows C (C[i - c0] = node
+ * i of level j-1) and level-j wavelet rows Dw (Dw[k - d0] = wavelet k). */
+int hwg_syn_stage(hwg_ctx *ctx, int j, const double *C, int64_t c0, const double *Dw, int64_t d0,
+                  double *Y, int64_t f0, int64_t nf, void *stream);
+
+/* Transposed stage j: C[i - c0] = (P_j^T x)[i] for i in [c0, c0 + nc) and
+ * Dw[k - d0] = (Q_j^T x)[k] for k in [d0, d0 + nd), from fine nodal rows X
+ * (X[f - x0] = node f of level j). */
+int hwg_ana_stage(hwg_ctx *ctx, int j, const double *X, int64_t x0, double *C, int64_t c0,
+                  int64_t nc, double *Dw, int64_t d0, int64_t nd, void *stream);
+
+/* B-side of the five-term S on nodal rows [r0, r0 + nr): t1 = A_t MxU + L^T
+ * AxU, t1' = M_t AxU + L MxU (system.py:119-139).  U holds nodal rows
+ * [u0, u0 + nu) including the halo rows the bands need.  If r0 == 0, E0
+ * (N_x, may be NULL) receives M_x U[0] for the trace term. */
+int hwg_bside_rows(hwg_ctx *ctx, const double *U, int64_t u0, int64_t nu, double *T1, double *T2,
+                   int64_t r0, int64_t nr, double *E0, void *stream);
+
+/* B^T-side: out = M_x G1 + A_x G2 on `rows` rows; E0 (or NULL) is added to
+ * the first row (only the rank that owns global row 0 passes it). */
+int hwg_bt_rows(hwg_ctx *ctx, const double *G1, const double *G2, const double *E0, double *out,
+                int64_t rows, void *stream);
+
+/* Batched V-cycles with a DEVICE array of per-row operator ids. */
+int hwg_mg_rows_dev(hwg_ctx *ctx, const int32_t *ops, const double *B, double *X, int64_t rows,
+                    void *stream);
+
+/* Per-row partial inner products part[r] = sum_i X[r,i] Y[r,i] (device). */
+int hwg_row_partials(hwg_ctx *ctx, const double *X, const double *Y, int64_t rows, double *part,
+                     void *stream);
+
+/* Fixed pairwise tree over n partials (solver.py:111-119) -> *result (device). */
+int hwg_tree_sum(hwg_ctx *ctx, const double *part, int64_t n, double *result, void *stream);
+
+/* Y += a X and Y = X + a Y over n values (axpy_rows / xpay_rows,
+ * _kernels.py:64-76). */
+int hwg_axpy(hwg_ctx *ctx, double a, const double *X, double *Y, int64_t n, void *stream);
+int hwg_xpay(hwg_ctx *ctx, double a, const double *X, double *Y, int64_t n, void *stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,9 @@ COEF_STRIDE = 8
 EXPORTS = ("hwg_last_error", "hwg_version", "hwg_create", "hwg_destroy",
            "hwg_workspace_bytes", "hwg_wavelet", "hwg_spatial", "hwg_schur_apply",
            "hwg_kx_apply", "hwg_mg_rows", "hwg_rhs", "hwg_dot", "hwg_pcg",
-           "hwg_solve_host", "hwg_launch_count", "hwg_profile_enable", "hwg_profile_read")
+           "hwg_solve_host", "hwg_launch_count", "hwg_profile_enable", "hwg_profile_read",
+           "hwg_syn_stage", "hwg_ana_stage", "hwg_bside_rows", "hwg_bt_rows", "hwg_mg_rows_dev",
+           "hwg_row_partials", "hwg_tree_sum", "hwg_axpy", "hwg_xpay")
 
 _P = C.c_void_p
 _D = C.c_double
@@ -35,7 +37,7 @@ class HwgDesc(C.Structure):
     _fields_ = [("dim", _I32), ("J", _I32), ("K", _I32), ("vcycles", _I32),
                 ("smooth", _I32), ("device", _I32), ("alpha", _D),
                 ("coef", _P), ("stencil_M", _P), ("stencil_A", _P),
-                ("temporal", _P), ("wavelet_scale", _P)]
+                ("temporal", _P), ("wavelet_scale", _P), ("rows_max", _I64)]
 
 
 class HwgPcgStats(C.Structure):
@@ -86,6 +88,15 @@ def load(build_if_missing=True):
     L.hwg_pcg.argtypes = [_P, _P, _P, _D, _D, _I32, _I32, C.POINTER(HwgPcgStats), _P]
     L.hwg_profile_enable.argtypes = [_P, C.c_int]
     L.hwg_profile_read.argtypes = [_P, C.c_int, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64)]
+    L.hwg_syn_stage.argtypes = [_P, C.c_int, _P, _I64, _P, _I64, _P, _I64, _I64, _P]
+    L.hwg_ana_stage.argtypes = [_P, C.c_int, _P, _I64, _P, _I64, _I64, _P, _I64, _I64, _P]
+    L.hwg_bside_rows.argtypes = [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P]
+    L.hwg_bt_rows.argtypes = [_P, _P, _P, _P, _P, _I64, _P]
+    L.hwg_mg_rows_dev.argtypes = [_P, _P, _P, _P, _I64, _P]
+    L.hwg_row_partials.argtypes = [_P, _P, _P, _I64, _P, _P]
+    L.hwg_tree_sum.argtypes = [_P, _P, _I64, _P, _P]
+    L.hwg_axpy.argtypes = [_P, _D, _P, _P, _I64, _P]
+    L.hwg_xpay.argtypes = [_P, _D, _P, _P, _I64, _P]
     L.hwg_solve_host.argtypes = [_P, _P, _P, _D, _D, _I32, _I32, C.POINTER(HwgPcgStats), _P]
     for name in EXPORTS:
         if name not in ("hwg_last_error", "hwg_version", "hwg_workspace_bytes",

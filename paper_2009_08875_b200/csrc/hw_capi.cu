@@ -55,6 +55,8 @@ struct hwg_ctx {
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx
     int64_t rows_max = 0;              // MG batch capacity (rows)
+    bool kernel_only = false;          // distributed-path context (no operator buffers)
+    int64_t red_max = 0;               // capacity of the dot partial / tree scratch
     Grid grid{};
     Stencil SM{}, SA{};
     std::vector<double> coef_host;
@@ -353,8 +355,8 @@ static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
     TRY(wavelet(c, X, c->U, c->T12, c->T12 + N, false, st));
     // t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU (one pass over U); the
     // first row of MxU is kept for the trace term
-    CK(launch_bside_fused(c->U, c->T12, c->T12 + N, c->MxU, c->grid, c->SM, c->SA, c->At.view(),
-                          c->LT.view(), c->Mt.view(), c->L.view(), nt, st));
+    CK(launch_bside_fused(c->U, 0, c->T12, c->T12 + N, c->MxU, c->grid, c->SM, c->SA,
+                          c->At.view(), c->LT.view(), c->Mt.view(), c->L.view(), 0, nt, nt, st));
     ++c->launches;
     TRY(mg_apply(c, c->T12, c->G12, 2 * nt, 0, nullptr, st));
     CK(launch_bt_side(c->G12, c->G12 + N, c->MxU, c->U, c->grid, c->SM, c->SA, nt, st));
@@ -391,7 +393,7 @@ static int ensure_pcg(hwg_ctx *c)
 extern "C" {
 
 const char *hwg_last_error(void) { return g_err.c_str(); }
-int hwg_version(void) { return 1; }
+int hwg_version(void) { return 2; }
 
 int hwg_create(const hwg_desc *desc, hwg_ctx **out)
 {
@@ -417,7 +419,8 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     c->nt = (1LL << d.J) + 1;
     c->nx = d.dim == 2 ? (int64_t)c->m * c->m : c->m;
     c->N = c->nt * c->nx;
-    c->rows_max = 2 * c->nt;
+    c->rows_max = d.rows_max > 0 ? d.rows_max : 2 * c->nt;
+    c->kernel_only = d.rows_max > 0;
     c->grid = Grid{d.dim, c->m, c->nx};
     c->SM = Stencil{d.stencil_M[0], d.stencil_M[1], d.stencil_M[2], d.stencil_M[3]};
     c->SA = Stencil{d.stencil_A[0], d.stencil_A[1], d.stencil_A[2], d.stencil_A[3]};
@@ -441,11 +444,13 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     for (int64_t r = 0; r < c->nt; ++r) ops[r] = 1 + c->level_of[r];
     GO(upload(c, &c->row_op_kx, ops));
     GO(build_temporal(c));
-    GO(dalloc(c, &c->U, c->N));
-    GO(dalloc(c, &c->MxU, c->N));
-    GO(dalloc(c, &c->AxU, c->N));
-    GO(dalloc(c, &c->T12, 2 * c->N));
-    GO(dalloc(c, &c->G12, 2 * c->N));
+    if (!c->kernel_only) {
+        GO(dalloc(c, &c->U, c->N));
+        GO(dalloc(c, &c->MxU, c->N));
+        GO(dalloc(c, &c->AxU, c->N));
+        GO(dalloc(c, &c->T12, 2 * c->N));
+        GO(dalloc(c, &c->G12, 2 * c->N));
+    }
     c->mgX.assign(d.K + 1, nullptr);
     c->mgB.assign(d.K + 1, nullptr);
     if (d.dim == 2 && d.K > kCoarseTop2d) {
@@ -454,8 +459,9 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
             GO(dalloc(c, &c->mgB[l], c->rows_max * level_size(c, l)));
         }
     }
-    GO(dalloc(c, &c->part, c->rows_max + 8));
-    GO(dalloc(c, &c->tmp, c->rows_max + 8));
+    c->red_max = std::max<int64_t>(c->rows_max, c->nt) + 8;   // dot partials / tree scratch
+    GO(dalloc(c, &c->part, c->red_max));
+    GO(dalloc(c, &c->tmp, c->red_max));
     GO(dalloc(c, &c->scal, 16));
     {
         void *q = nullptr;
@@ -514,6 +520,7 @@ int64_t hwg_launch_count(const hwg_ctx *c) { return c ? c->launches : 0; }
 int hwg_wavelet(hwg_ctx *c, const double *X, double *Y, int transpose, void *stream)
 {
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (X == Y) return fail(HWG_EINVAL, "wavelet input and output may not alias");
     TRY(wavelet(c, X, Y, c->T12, c->T12 + c->N, transpose != 0, S(stream)));
     return HWG_OK;
@@ -531,12 +538,14 @@ int hwg_spatial(hwg_ctx *c, int which, const double *X, double *Y, int64_t rows,
 int hwg_schur_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 {
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     return schur(c, X, Y, S(stream));
 }
 
 int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 {
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (X == Y) return fail(HWG_EINVAL, "K_X input and output may not alias");
     return kx(c, X, Y, S(stream));
 }
@@ -563,6 +572,7 @@ int hwg_rhs(hwg_ctx *c, const double *F, const double *load, const double *u0pro
             double *fhat, void *stream)
 {
     if (!c || !fhat) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     cudaStream_t st = S(stream);
     const int64_t nt = c->nt, nx = c->nx, N = c->N, ntest = 2 * (nt - 1);
     // g part: W^T (T^T (x) M_x + N^T (x) A_x) K_Y y, y = (N (x) M_x) F
@@ -613,6 +623,7 @@ int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
             int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out, void *stream)
 {
     if (!c || !f || !w) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (!(epsilon > 0) && !(rtol > 0)) return fail(HWG_EINVAL, "tolerance must be positive");
     if (max_iterations < 0 || recompute_every < 1) return fail(HWG_EINVAL, "bad iteration limits");
     TRY(ensure_pcg(c));
@@ -735,6 +746,7 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
                    hwg_pcg_stats *stats, void *stream)
 {
     if (!c || !fhat_host || !u_host) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     cudaStream_t st = S(stream);
     if (!c->fdev) {
         TRY(dalloc(c, &c->fdev, c->N));
@@ -747,6 +759,92 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
     CK(cudaMemcpyAsync(u_host, c->U, c->N * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return rc;
+}
+
+// ---- time-slab building blocks --------------------------------------------
+int hwg_syn_stage(hwg_ctx *c, int j, const double *C, int64_t c0, const double *Dw, int64_t d0,
+                  double *Y, int64_t f0, int64_t nf, void *stream)
+{
+    if (!c || !C || !Dw || !Y || j < 1 || j > c->J || nf < 0) return fail(HWG_EINVAL, "bad argument");
+    CK(launch_syn_stage(j, c->scale[j - 1], C, c0, Dw, d0, Y, f0, nf, c->nx, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_ana_stage(hwg_ctx *c, int j, const double *X, int64_t x0, double *C, int64_t c0,
+                  int64_t nc, double *Dw, int64_t d0, int64_t nd, void *stream)
+{
+    if (!c || !X || (nc && !C) || (nd && !Dw) || j < 1 || j > c->J || nc < 0 || nd < 0)
+        return fail(HWG_EINVAL, "bad argument");
+    CK(launch_ana_stage(j, c->scale[j - 1], X, x0, C, c0, nc, Dw, d0, nd, c->nx, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_bside_rows(hwg_ctx *c, const double *U, int64_t u0, int64_t nu, double *T1, double *T2,
+                   int64_t r0, int64_t nr, double *E0, void *stream)
+{
+    if (!c || !U || !T1 || !T2 || nr < 0 || r0 < 0 || r0 + nr > c->nt) return fail(HWG_EINVAL, "bad argument");
+    if (u0 > (r0 > 0 ? r0 - 1 : 0) || u0 + nu < (r0 + nr < c->nt ? r0 + nr + 1 : r0 + nr))
+        return fail(HWG_EINVAL, "U does not cover the rows the temporal bands need");
+    if (nr == 0) return HWG_OK;
+    CK(launch_bside_fused(U, u0, T1, T2, r0 == 0 ? E0 : nullptr, c->grid, c->SM, c->SA,
+                          c->At.view(), c->LT.view(), c->Mt.view(), c->L.view(), r0, nr, c->nt,
+                          S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_bt_rows(hwg_ctx *c, const double *G1, const double *G2, const double *E0, double *out,
+                int64_t rows, void *stream)
+{
+    if (!c || !G1 || !G2 || !out || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    if (rows == 0) return HWG_OK;
+    CK(launch_bt_side(G1, G2, E0, out, c->grid, c->SM, c->SA, rows, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_mg_rows_dev(hwg_ctx *c, const int32_t *ops, const double *B, double *X, int64_t rows,
+                    void *stream)
+{
+    if (!c || !ops || !B || !X || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
+    if (rows == 0) return HWG_OK;
+    return mg_apply(c, B, X, rows, 0, ops, S(stream));
+}
+
+int hwg_row_partials(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *part,
+                     void *stream)
+{
+    if (!c || !X || !Y || !part || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    CK(launch_row_partials(X, Y, rows, c->nx, part, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_tree_sum(hwg_ctx *c, const double *part, int64_t n, double *result, void *stream)
+{
+    if (!c || !part || !result || n < 0 || n + 4 > c->red_max) return fail(HWG_EINVAL, "bad argument");
+    CK(launch_tree(part, n, c->tmp, result, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_axpy(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *stream)
+{
+    if (!c || !X || !Y || n < 0) return fail(HWG_EINVAL, "bad argument");
+    CK(launch_axpy(a, X, Y, n, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_xpay(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *stream)
+{
+    if (!c || !X || !Y || n < 0) return fail(HWG_EINVAL, "bad argument");
+    CK(launch_xpay(a, X, Y, n, S(stream)));
+    ++c->launches;
+    return HWG_OK;
 }
 
 }  // extern "C"

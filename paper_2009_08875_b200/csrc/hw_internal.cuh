@@ -57,6 +57,12 @@ cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
 cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
                           const double *scale, int64_t nt, int64_t nx, bool transpose,
                           cudaStream_t st, int64_t *launches);
+cudaError_t launch_syn_stage(int j, double s, const double *C, int64_t c0, const double *Dm,
+                             int64_t d0, double *Y, int64_t f0, int64_t nf, int64_t nx,
+                             cudaStream_t st);
+cudaError_t launch_ana_stage(int j, double s, const double *X, int64_t x0, double *C, int64_t c0,
+                             int64_t nc, double *Dm, int64_t d0, int64_t nd, int64_t nx,
+                             cudaStream_t st);
 
 // ---- hw_kron.cu ----------------------------------------------------------
 struct Stencil {           // finest-level spatial stencil, see hwg_desc
@@ -82,9 +88,9 @@ cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0,
                            Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st);
 cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx,
                                   cudaStream_t st);
-cudaError_t launch_bside_fused(const double *U, double *T1, double *T2, double *E0, Grid g,
-                               Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
-                               int64_t nt, cudaStream_t st);
+cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *T2, double *E0,
+                               Grid g, Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
+                               int64_t r0, int64_t nr, int64_t nt, cudaStream_t st);
 cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
                        cudaStream_t st);
 
@@ -99,5 +105,10 @@ cudaError_t launch_update_p(double *p, const double *z, const double *s, int64_t
                             cudaStream_t st);
 cudaError_t launch_sub(const double *f, const double *t, double *r, int64_t n, cudaStream_t st);
 cudaError_t launch_any_nonzero(const double *X, int64_t n, int *flag, cudaStream_t st);
+cudaError_t launch_row_partials(const double *X, const double *Y, int64_t rows, int64_t nx,
+                                double *part, cudaStream_t st);
+cudaError_t launch_tree(const double *part, int64_t n, double *tmp, double *out, cudaStream_t st);
+cudaError_t launch_axpy(double a, const double *X, double *Y, int64_t n, cudaStream_t st);
+cudaError_t launch_xpay(double a, const double *X, double *Y, int64_t n, cudaStream_t st);
 
 }  // namespace hw

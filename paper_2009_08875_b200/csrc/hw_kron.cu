@@ -133,35 +133,40 @@ __device__ __forceinline__ double band3(const TCsr &B, int64_t c, double vm, dou
 // MxU = M_x U, AxU = A_x U computed on the fly (system.py:119-139).  Each CTA
 // owns a spatial tile and a chunk of temporal rows and slides a 3-row window
 // of (MxU, AxU) in registers, so U is read once and t1, t1' written once.
-// E0 (optional) receives M_x U[0] for the trace term.
-__global__ void __launch_bounds__(TX * TY) bside_fused(const double *__restrict__ U,
+// Output rows are the global temporal rows [r0, r0 + nr) (T1/T2 indexed from
+// r0); U holds global rows [u0, ...) including the halo rows the bands touch;
+// nt is the global row count.  E0 (optional) receives M_x U[0].
+__global__ void __launch_bounds__(TX * TY) bside_fused(const double *__restrict__ U, int64_t u0,
                                                        double *__restrict__ T1,
                                                        double *__restrict__ T2,
                                                        double *__restrict__ E0, Grid g,
                                                        Stencil M, Stencil A, TCsr At, TCsr LT,
-                                                       TCsr Mt, TCsr Lm, int64_t nt, int chunk)
+                                                       TCsr Mt, TCsr Lm, int64_t r0, int64_t nr,
+                                                       int64_t nt, int chunk)
 {
     const Pt p = point_of(g);
     if (!p.ok) return;
     const int64_t k = pidx(p, g);
-    for (int64_t c0 = (int64_t)blockIdx.z * chunk; c0 < nt; c0 += (int64_t)gridDim.z * chunk) {
-        const int64_t c1 = c0 + chunk < nt ? c0 + chunk : nt;
+    auto urow = [&](int64_t c) { return U + (c - u0) * g.nx; };
+    for (int64_t c0 = r0 + (int64_t)blockIdx.z * chunk; c0 < r0 + nr;
+         c0 += (int64_t)gridDim.z * chunk) {
+        const int64_t c1 = c0 + chunk < r0 + nr ? c0 + chunk : r0 + nr;
         double mm = 0.0, am = 0.0;                     // row c-1
         if (c0 > 0) {
-            mm = stencil_pt(U + (c0 - 1) * g.nx, p, g, M);
-            am = stencil_pt(U + (c0 - 1) * g.nx, p, g, A);
+            mm = stencil_pt(urow(c0 - 1), p, g, M);
+            am = stencil_pt(urow(c0 - 1), p, g, A);
         }
-        double m0 = stencil_pt(U + c0 * g.nx, p, g, M);
-        double a0 = stencil_pt(U + c0 * g.nx, p, g, A);
+        double m0 = stencil_pt(urow(c0), p, g, M);
+        double a0 = stencil_pt(urow(c0), p, g, A);
         if (c0 == 0 && E0) E0[k] = m0;
         for (int64_t c = c0; c < c1; ++c) {
             double mp = 0.0, ap = 0.0;                 // row c+1
             if (c + 1 < nt) {
-                mp = stencil_pt(U + (c + 1) * g.nx, p, g, M);
-                ap = stencil_pt(U + (c + 1) * g.nx, p, g, A);
+                mp = stencil_pt(urow(c + 1), p, g, M);
+                ap = stencil_pt(urow(c + 1), p, g, A);
             }
-            T1[c * g.nx + k] = add_rn(band3(At, c, mm, m0, mp), band3(LT, c, am, a0, ap));
-            T2[c * g.nx + k] = add_rn(band3(Mt, c, am, a0, ap), band3(Lm, c, mm, m0, mp));
+            T1[(c - r0) * g.nx + k] = add_rn(band3(At, c, mm, m0, mp), band3(LT, c, am, a0, ap));
+            T2[(c - r0) * g.nx + k] = add_rn(band3(Mt, c, am, a0, ap), band3(Lm, c, mm, m0, mp));
             mm = m0; am = a0;
             m0 = mp; a0 = ap;
         }
@@ -225,19 +230,20 @@ cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0,
     return cudaGetLastError();
 }
 
-cudaError_t launch_bside_fused(const double *U, double *T1, double *T2, double *E0, Grid g,
-                               Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
-                               int64_t nt, cudaStream_t st)
+cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *T2, double *E0,
+                               Grid g, Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
+                               int64_t r0, int64_t nr, int64_t nt, cudaStream_t st)
 {
     // temporal chunks: enough CTAs for ~8 per SM, at least 8 rows per chunk
     dim3 grid = spatial_grid(g, 1);
     const int64_t tiles = (int64_t)grid.x * grid.y;
     int64_t chunks = (148LL * 8 + tiles - 1) / tiles;
-    int chunk = (int)((nt + chunks - 1) / chunks);
+    int chunk = (int)((nr + chunks - 1) / chunks);
     if (chunk < 8) chunk = 8;
-    chunks = (nt + chunk - 1) / chunk;
-    grid.z = (unsigned)(chunks < 65535 ? chunks : 65535);
-    bside_fused<<<grid, dim3(TX, TY), 0, st>>>(U, T1, T2, E0, g, M, A, At, LT, Mt, L, nt, chunk);
+    chunks = (nr + chunk - 1) / chunk;
+    grid.z = (unsigned)(chunks < 65535 ? (chunks < 1 ? 1 : chunks) : 65535);
+    bside_fused<<<grid, dim3(TX, TY), 0, st>>>(U, u0, T1, T2, E0, g, M, A, At, LT, Mt, L, r0, nr,
+                                               nt, chunk);
     return cudaGetLastError();
 }
 

@@ -129,6 +129,46 @@ cudaError_t launch_dot(const double *X, const double *Y, int64_t rows, int64_t n
     return cudaGetLastError();
 }
 
+cudaError_t launch_row_partials(const double *X, const double *Y, int64_t rows, int64_t nx,
+                                double *part, cudaStream_t st)
+{
+    if (rows <= 0) return cudaSuccess;
+    row_dots<256><<<(unsigned)rows, 256, 0, st>>>(X, Y, part, nx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tree(const double *part, int64_t n, double *tmp, double *out, cudaStream_t st)
+{
+    tree_reduce2<<<1, 1024, 0, st>>>(part, n, tmp, out);
+    return cudaGetLastError();
+}
+
+// Y += a X (axpy_rows) and Y = X + a Y (xpay_rows) with a host scalar
+__global__ void axpy_h(double a, const double *__restrict__ X, double *__restrict__ Y, int64_t n)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        Y[e] = add_rn(Y[e], mul_rn(a, X[e]));
+}
+__global__ void xpay_h(double a, const double *__restrict__ X, double *__restrict__ Y, int64_t n)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        Y[e] = add_rn(X[e], mul_rn(a, Y[e]));
+}
+
+cudaError_t launch_axpy(double a, const double *X, double *Y, int64_t n, cudaStream_t st)
+{
+    axpy_h<<<grid_for(n, 256), 256, 0, st>>>(a, X, Y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xpay(double a, const double *X, double *Y, int64_t n, cudaStream_t st)
+{
+    xpay_h<<<grid_for(n, 256), 256, 0, st>>>(a, X, Y, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pcg_alpha(double *s, cudaStream_t st)
 {
     pcg_alpha<<<1, 1, 0, st>>>(s);

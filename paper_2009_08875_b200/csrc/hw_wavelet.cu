@@ -24,57 +24,65 @@ namespace hw {
 __device__ __forceinline__ double qa(double s, int k) { return s * (k == 0 ? -1.0 : -0.5); }
 __device__ __forceinline__ double qb(double s, int k, int nw) { return s * (k == nw - 1 ? -1.0 : -0.5); }
 
-// dst rows [0, nf) <- M_j [c ; d]; grid: (column blocks, stage rows)
-__global__ void wav_syn_stage(const double *__restrict__ C, const double *__restrict__ Dm,
-                              double *__restrict__ Y, int j, double s, int64_t nx)
+// Y[f - f0] <- (M_j [c ; d])[f] for fine nodes f in [f0, f0 + nf);
+// C[i - c0] = coarse node i, Dm[k - d0] = level-j wavelet k.
+// grid: (column blocks, output rows)
+__global__ void wav_syn_stage(const double *__restrict__ C, int64_t c0, const double *__restrict__ Dm,
+                              int64_t d0, double *__restrict__ Y, int64_t f0, int64_t nf, int j,
+                              double s, int64_t nx)
 {
-    const int nc = (1 << (j - 1)) + 1, nf = (1 << j) + 1, nw = 1 << (j - 1);
+    const int nw = 1 << (j - 1);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nx) return;
-    for (int r = blockIdx.y; r < nf; r += gridDim.y) {
+    for (int64_t rr = blockIdx.y; rr < nf; rr += gridDim.y) {
+        const int64_t r = f0 + rr;                 // global fine node
         double acc;
         if ((r & 1) == 0) {
-            const int q = r >> 1;                 // coarse index
-            acc = C[(int64_t)q * nx + i];         // P: 1.0 * c[q]
-            if (q >= 1)                           // Q col q-1: s * b_{q-1}
-                acc = add_rn(acc, mul_rn(qb(s, q - 1, nw), Dm[(int64_t)(nc + q - 1) * nx + i]));
-            if (q < nw)                           // Q col q: s * a_q
-                acc = add_rn(acc, mul_rn(qa(s, q), Dm[(int64_t)(nc + q) * nx + i]));
+            const int q = (int)(r >> 1);           // coarse index
+            acc = C[(q - c0) * nx + i];            // P: 1.0 * c[q]
+            if (q >= 1)                            // Q col q-1: s * b_{q-1}
+                acc = add_rn(acc, mul_rn(qb(s, q - 1, nw), Dm[(q - 1 - d0) * nx + i]));
+            if (q < nw)                            // Q col q: s * a_q
+                acc = add_rn(acc, mul_rn(qa(s, q), Dm[(q - d0) * nx + i]));
         } else {
-            const int k = r >> 1;
-            acc = mul_rn(0.5, C[(int64_t)k * nx + i]);
-            acc = add_rn(acc, mul_rn(0.5, C[(int64_t)(k + 1) * nx + i]));
-            acc = add_rn(acc, mul_rn(s, Dm[(int64_t)(nc + k) * nx + i]));
+            const int k = (int)(r >> 1);
+            acc = mul_rn(0.5, C[(k - c0) * nx + i]);
+            acc = add_rn(acc, mul_rn(0.5, C[(k + 1 - c0) * nx + i]));
+            acc = add_rn(acc, mul_rn(s, Dm[(k - d0) * nx + i]));
         }
-        Y[(int64_t)r * nx + i] = acc;
+        Y[rr * nx + i] = acc;
     }
 }
 
-// c' -> Cout rows [0, nc), d' -> Dout rows [nc, nf)   (M_j^T applied to X)
-__global__ void wav_ana_stage(const double *__restrict__ X, double *__restrict__ Cout,
-                              double *__restrict__ Dout, int j, double s, int64_t nx)
+// Cout[i - c0] = (P_j^T x)[i], i in [c0, c0 + nc); Dout[k - d0] = (Q_j^T x)[k],
+// k in [d0, d0 + nd); X[f - x0] = fine node f.  grid rows: nc + nd
+__global__ void wav_ana_stage(const double *__restrict__ X, int64_t x0, double *__restrict__ Cout,
+                              int64_t c0, int64_t nc, double *__restrict__ Dout, int64_t d0,
+                              int64_t nd, int j, double s, int64_t nx)
 {
-    const int nc = (1 << (j - 1)) + 1, nf = (1 << j) + 1, nw = 1 << (j - 1);
+    const int nf = (1 << j) + 1, nw = 1 << (j - 1);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nx) return;
-    for (int r = blockIdx.y; r < nf; r += gridDim.y) {
-        if (r < nc) {
-            // column r of P_j: rows 2r-1 (1/2), 2r (1), 2r+1 (1/2)
+    auto xr = [&](int64_t f) { return X[(f - x0) * nx + i]; };
+    for (int64_t rr = blockIdx.y; rr < nc + nd; rr += gridDim.y) {
+        if (rr < nc) {
+            const int64_t r = c0 + rr;             // column r of P_j: rows 2r-1 (1/2), 2r (1), 2r+1 (1/2)
             double acc;
             if (r >= 1) {
-                acc = mul_rn(0.5, X[(int64_t)(2 * r - 1) * nx + i]);
-                acc = add_rn(acc, X[(int64_t)(2 * r) * nx + i]);
+                acc = mul_rn(0.5, xr(2 * r - 1));
+                acc = add_rn(acc, xr(2 * r));
             } else {
-                acc = X[i];
+                acc = xr(0);
             }
-            if (2 * r + 1 < nf) acc = add_rn(acc, mul_rn(0.5, X[(int64_t)(2 * r + 1) * nx + i]));
-            Cout[(int64_t)r * nx + i] = acc;
+            if (2 * r + 1 < nf) acc = add_rn(acc, mul_rn(0.5, xr(2 * r + 1)));
+            Cout[rr * nx + i] = acc;
         } else {
-            const int k = r - nc;                 // column k of Q_j: rows 2k, 2k+1, 2k+2
-            double acc = mul_rn(qa(s, k), X[(int64_t)(2 * k) * nx + i]);
-            acc = add_rn(acc, mul_rn(s, X[(int64_t)(2 * k + 1) * nx + i]));
-            acc = add_rn(acc, mul_rn(qb(s, k, nw), X[(int64_t)(2 * k + 2) * nx + i]));
-            Dout[(int64_t)r * nx + i] = acc;
+            const int64_t kk = rr - nc;
+            const int k = (int)(d0 + kk);           // column k of Q_j: rows 2k, 2k+1, 2k+2
+            double acc = mul_rn(qa(s, k), xr(2 * k));
+            acc = add_rn(acc, mul_rn(s, xr(2 * k + 1)));
+            acc = add_rn(acc, mul_rn(qb(s, k, nw), xr(2 * k + 2)));
+            Dout[kk * nx + i] = acc;
         }
     }
 }
@@ -84,13 +92,29 @@ static dim3 stage_grid(int64_t rows, int64_t nx, int bs)
     return dim3((unsigned)((nx + bs - 1) / bs), (unsigned)(rows < 65535 ? rows : 65535));
 }
 
+cudaError_t launch_syn_stage(int j, double s, const double *C, int64_t c0, const double *Dm,
+                             int64_t d0, double *Y, int64_t f0, int64_t nf, int64_t nx,
+                             cudaStream_t st)
+{
+    wav_syn_stage<<<stage_grid(nf, nx, 256), 256, 0, st>>>(C, c0, Dm, d0, Y, f0, nf, j, s, nx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ana_stage(int j, double s, const double *X, int64_t x0, double *C, int64_t c0,
+                             int64_t nc, double *Dm, int64_t d0, int64_t nd, int64_t nx,
+                             cudaStream_t st)
+{
+    wav_ana_stage<<<stage_grid(nc + nd, nx, 256), 256, 0, st>>>(X, x0, C, c0, nc, Dm, d0, nd, j,
+                                                                  s, nx);
+    return cudaGetLastError();
+}
+
 // Y = W X (transpose = 0) or W^T X (transpose = 1).  S1 (and S2 for the
 // transpose) are scratch arrays with at least 2^(J-1)+1 rows.
 cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
                           const double *scale, int64_t nt, int64_t nx, bool transpose,
                           cudaStream_t st, int64_t *launches)
 {
-    const int bs = 256;
     if (J == 0) {
         return cudaMemcpyAsync(Y, X, (size_t)(nt * nx) * sizeof(double),
                                cudaMemcpyDeviceToDevice, st);
@@ -99,8 +123,10 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         const double *src = X;
         for (int j = 1; j <= J; ++j) {
             double *dst = ((J - j) % 2 == 0) ? Y : S1;
-            wav_syn_stage<<<stage_grid((1LL << j) + 1, nx, bs), bs, 0, st>>>(src, X, dst, j,
-                                                                          scale[j - 1], nx);
+            const int64_t nc = (1LL << (j - 1)) + 1;
+            cudaError_t e = launch_syn_stage(j, scale[j - 1], src, 0, X + nc * nx, 0, dst, 0,
+                                             (1LL << j) + 1, nx, st);
+            if (e != cudaSuccess) return e;
             ++*launches;
             src = dst;
         }
@@ -108,8 +134,10 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         const double *src = X;
         for (int j = J; j >= 1; --j) {
             double *cdst = (j == 1) ? Y : (((J - j) % 2 == 0) ? S1 : S2);
-            wav_ana_stage<<<stage_grid((1LL << j) + 1, nx, bs), bs, 0, st>>>(src, cdst, Y, j,
-                                                                          scale[j - 1], nx);
+            const int64_t nc = (1LL << (j - 1)) + 1;
+            cudaError_t e = launch_ana_stage(j, scale[j - 1], src, 0, cdst, 0, nc, Y + nc * nx, 0,
+                                             1LL << (j - 1), nx, st);
+            if (e != cudaSuccess) return e;
             ++*launches;
             src = cdst;
         }

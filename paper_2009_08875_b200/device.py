@@ -53,7 +53,7 @@ class GpuContext:
     """Owns one hwg_ctx: tables, workspaces and the launch counter."""
 
     def __init__(self, d, J, K, alpha=0.3, vcycles=2, smooth=3, D=None, c=0.0,
-                 device=0, coef=None):
+                 device=0, coef=None, rows_max=0):
         self.device = require_cuda(device)
         self.lib = _lib.load()
         self.d, self.J, self.K = d, J, K
@@ -73,7 +73,7 @@ class GpuContext:
                             coef=self.coef.ctypes.data, stencil_M=self.stencil_M.ctypes.data,
                             stencil_A=self.stencil_A.ctypes.data,
                             temporal=self.temporal.ctypes.data,
-                            wavelet_scale=self.scales.ctypes.data)
+                            wavelet_scale=self.scales.ctypes.data, rows_max=int(rows_max))
         h = C.c_void_p()
         _lib.check(self.lib.hwg_create(C.byref(desc), C.byref(h)))
         self.handle = h
@@ -111,6 +111,43 @@ class GpuContext:
                                                  C.byref(n)))
             out[name] = (ms.value, by.value, n.value)
         return out
+
+    # ---- time-slab building blocks (distributed path) ----------------------
+    def syn_stage(self, j, C, c0, Dw, d0, Y, f0, nf):
+        _lib.check(self.lib.hwg_syn_stage(self.handle, j, ptr(C), c0, ptr(Dw), d0, ptr(Y), f0, nf,
+                                          self.stream()))
+
+    def ana_stage(self, j, X, x0, C, c0, nc, Dw, d0, nd):
+        _lib.check(self.lib.hwg_ana_stage(self.handle, j, ptr(X), x0,
+                                          ptr(C) if nc else None, c0, nc,
+                                          ptr(Dw) if nd else None, d0, nd, self.stream()))
+
+    def bside_rows(self, U, u0, T1, T2, r0, nr, E0=None):
+        _lib.check(self.lib.hwg_bside_rows(self.handle, ptr(U), u0, U.shape[0], ptr(T1), ptr(T2),
+                                           r0, nr, ptr(E0) if E0 is not None else None,
+                                           self.stream()))
+
+    def bt_rows(self, G1, G2, E0, out):
+        _lib.check(self.lib.hwg_bt_rows(self.handle, ptr(G1), ptr(G2),
+                                        ptr(E0) if E0 is not None else None, ptr(out),
+                                        out.shape[0], self.stream()))
+
+    def mg_rows_dev(self, ops, B, X):
+        _lib.check(self.lib.hwg_mg_rows_dev(self.handle, ptr(ops), ptr(B), ptr(X), B.shape[0],
+                                            self.stream()))
+
+    def row_partials(self, X, Y, part):
+        _lib.check(self.lib.hwg_row_partials(self.handle, ptr(X), ptr(Y), X.shape[0], ptr(part),
+                                             self.stream()))
+
+    def tree_sum(self, part, n, out):
+        _lib.check(self.lib.hwg_tree_sum(self.handle, ptr(part), n, ptr(out), self.stream()))
+
+    def axpy(self, a, X, Y):
+        _lib.check(self.lib.hwg_axpy(self.handle, float(a), ptr(X), ptr(Y), X.numel(), self.stream()))
+
+    def xpay(self, a, X, Y):
+        _lib.check(self.lib.hwg_xpay(self.handle, float(a), ptr(X), ptr(Y), X.numel(), self.stream()))
 
     def wavelet(self, X, Y, transpose):
         _lib.check(self.lib.hwg_wavelet(self.handle, ptr(X), ptr(Y), int(transpose), self.stream()))

@@ -1,0 +1,481 @@
+"""Time-slab multi-GPU PCG (design (a)).
+
+The reference distributes temporal rows over a thread pool with halo reads
+(ParallelPlan / WorkerPool, /root/reference/pkg/src/heatwave/solver.py:
+47-108); the paper distributes them over MPI ranks.  Here
+P = 2^L0 GPUs each own a time slab:
+
+* nodal rows (single-scale arrays of S): rank p owns nodes [pH, (p+1)H),
+  H = 2^J / P, and the last rank also owns the end node 2^J;
+* wavelet rows (PCG vectors, K_X): levels j <= L0 (the P + 1 coarsest rows)
+  are REPLICATED on every rank; for j > L0 rank p owns the level-j wavelets
+  centred in its slab, k in [p 2^(j-1)/P, (p+1) 2^(j-1)/P).
+
+Exchanges per PCG iteration: one coarse-node and one wavelet halo row per
+distributed synthesis stage, one halo row on each side for the temporal
+bands of S, one fine-node halo on each side per transposed stage, an
+allgather of the P + 1 level-L0 nodal rows, and an allgather of the per-row
+dot partials.  The partials are reassembled in GLOBAL row order and reduced
+with the reference's fixed pairwise tree on every rank, so inner products
+(hence iterates and iteration counts) are identical for every P -- the
+reference's worker-count determinism (tests/test_solver.py:129-142).  K_X
+and every multigrid solve are row-local: no communication.
+
+The code is SPMD over a list of rank states.  A real run holds its own
+state and a ``TorchComm`` (NCCL between GPUs, gloo on CPUs); ``SimComm``
+holds all P states in one process and delivers messages by copying, which
+runs P virtual ranks one after another on one device (the tests; no kernel
+ever waits for another rank).  Every exchange is a pure function of (rank
+layout, stage) -> [Msg], so a real rank derives the receives it must post
+from its neighbours' plans without seeing their data.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Callable, List, NamedTuple
+
+import numpy as np
+
+from . import discretization as disc
+
+
+# --------------------------------------------------------------------------
+# partition
+# --------------------------------------------------------------------------
+@dataclass
+class RankLayout:
+    p: int
+    P: int
+    J: int
+    H: int
+    L0: int
+    last: bool
+    n_out: int                    # nodal rows owned (H, +1 on the last rank)
+    n_w: int                      # wavelet rows held (P + 1 replicated + H - 1 own)
+    global_rows: np.ndarray       # global wavelet row of each local row
+    owned: np.ndarray             # counts in dots (replicated rows only on rank 0)
+    level_of: np.ndarray          # wavelet level of each local row
+    block: dict                   # level j > L0 -> (local start, count)
+
+    @property
+    def left(self):
+        return self.p - 1 if self.p > 0 else None
+
+    @property
+    def right(self):
+        return self.p + 1 if not self.last else None
+
+
+_LAYOUTS = {}
+
+
+def slab_layout(J: int, P: int, p: int) -> RankLayout:
+    key = (J, P, p)
+    if key in _LAYOUTS:
+        return _LAYOUTS[key]
+    if P < 1 or P & (P - 1):
+        raise ValueError("the number of ranks must be a power of two")
+    if P > 2 ** (J - 1):
+        raise ValueError(f"at most 2^(J-1) = {2 ** (J - 1)} ranks for J = {J}")
+    if not 0 <= p < P:
+        raise ValueError("rank out of range")
+    L0 = P.bit_length() - 1
+    H = 2 ** J // P
+    rows = list(range(P + 1))
+    block = {}
+    for j in range(L0 + 1, J + 1):
+        n = 2 ** (j - 1) // P
+        block[j] = (len(rows), n)
+        rows.extend(2 ** (j - 1) + 1 + p * n + k for k in range(n))
+    g = np.array(rows, dtype=np.int64)
+    owned = np.ones(len(g), dtype=bool)
+    if p > 0:
+        owned[:P + 1] = False
+    last = p == P - 1
+    lay = RankLayout(p, P, J, H, L0, last, H + (1 if last else 0), len(g), g, owned,
+                     disc.level_of(J)[g], block)
+    _LAYOUTS[key] = lay
+    return lay
+
+
+class Msg(NamedTuple):
+    src: str          # source buffer name on the sending rank
+    src_row: int
+    dst: int          # destination rank
+    dst_buf: str
+    dst_row: int
+
+
+# stage buffers share one layout: [left halo | own rows | right slot]
+def _syn_buf(j, J):
+    return "U" if j == J else ("B1" if (J - j) % 2 else "B2")
+
+
+def _ana_buf(j, J):
+    return "Xa" if j == J else ("B1" if (J - j) % 2 else "B2")
+
+
+def edge_plan(lay: RankLayout, buf: str, n_own: int) -> List[Msg]:
+    """First own row -> left neighbour's slot; last own row -> right
+    neighbour's left halo (both buffers laid out [halo | n_own | slot])."""
+    out = []
+    if lay.left is not None:
+        out.append(Msg(buf, 1, lay.left, buf, n_own + 1))
+    if lay.right is not None:
+        out.append(Msg(buf, n_own, lay.right, buf, 0))
+    return out
+
+
+def syn_plan(lay: RankLayout, j: int) -> List[Msg]:
+    """Halos of synthesis stage j > L0: my first coarse node (row 1 of the
+    previous stage's output) to the left neighbour's slot, my last level-j
+    wavelet to the right neighbour's wavelet halo."""
+    out = []
+    n_c = 2 ** (j - 1) // lay.P
+    if j > lay.L0 + 1 and lay.left is not None:
+        prev = _syn_buf(j - 1, lay.J)
+        out.append(Msg(prev, 1, lay.left, prev, n_c + 1))
+    if lay.right is not None:
+        off, n = lay.block[j]
+        out.append(Msg("X", off + n - 1, lay.right, "D", 0))
+    return out
+
+
+# --------------------------------------------------------------------------
+# communicators
+# --------------------------------------------------------------------------
+class SimComm:
+    """All ranks in one process; messages are device copies."""
+
+    def __init__(self, P):
+        self.P = P
+
+    def exchange(self, states, plan: Callable[[RankLayout], List[Msg]]):
+        for st in states:
+            for m in plan(st.lay):
+                states[m.dst].bufs[m.dst_buf][m.dst_row].copy_(st.bufs[m.src][m.src_row])
+
+    def allgather(self, states, tensors):
+        import torch
+        stacked = torch.stack(list(tensors))
+        return [stacked for _ in states]
+
+
+class TorchComm:
+    """torch.distributed process group (NCCL between GPUs, gloo on CPUs)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+        self.P = dist.get_world_size()
+        self.rank = dist.get_rank()
+
+    def exchange(self, states, plan):
+        dist = self.dist
+        (st,) = states
+        lay = st.lay
+        ops = []
+        for m in plan(lay):
+            ops.append(dist.P2POp(dist.isend, st.bufs[m.src][m.src_row].contiguous(), m.dst))
+        for q in (lay.left, lay.right):
+            if q is None:
+                continue
+            for m in plan(slab_layout(lay.J, lay.P, q)):
+                if m.dst == lay.p:
+                    ops.append(dist.P2POp(dist.irecv, st.bufs[m.dst_buf][m.dst_row], q))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allgather(self, states, tensors):
+        import torch
+        (t,) = tensors
+        out = [torch.empty_like(t) for _ in range(self.P)]
+        self.dist.all_gather(out, t.contiguous())
+        return [torch.stack(out)]
+
+
+# --------------------------------------------------------------------------
+# per-rank state
+# --------------------------------------------------------------------------
+class RankState:
+    """Buffers of one rank.  ``kern`` provides the local kernels (the C ABI's
+    time-slab entry points via GpuContext, or a test double)."""
+
+    def __init__(self, lay: RankLayout, kern, n_x, device, dtype=None):
+        import torch
+        dtype = dtype or torch.float64
+        self.lay = lay
+        self.k = kern
+        H = lay.H
+        z = lambda r: torch.zeros((r, n_x), dtype=dtype, device=device)  # noqa: E731
+        self.bufs = {"U": z(H + 2), "Xa": z(H + 2), "B1": z(H + 2), "B2": z(H + 2),
+                     "D": z(H // 2 + 2), "X": None}
+        self.CN = [z(2 ** j + 1) for j in range(lay.L0 + 1)]     # replicated coarse nodal
+        self.T12 = z(2 * lay.n_out)
+        self.G12 = z(2 * lay.n_out)
+        self.E0 = z(1)[0] if lay.p == 0 else None
+        self.mid = z(lay.n_w)
+        self.part = torch.zeros(lay.n_w, dtype=dtype, device=device)
+        self.owned = torch.as_tensor(lay.owned.astype(np.float64), dtype=dtype, device=device)
+        self.ops_kx = torch.as_tensor(1 + lay.level_of, dtype=torch.int32, device=device)
+        self.ops_zero = torch.zeros(2 * lay.n_out, dtype=torch.int32, device=device)
+        # global-order assembly of dot partials (same on every rank)
+        J, P = lay.J, lay.P
+        src_idx, dst_idx = [], []
+        for q in range(P):
+            lq = slab_layout(J, P, q)
+            own = np.nonzero(lq.owned)[0]
+            src_idx.append(q * lq.n_w + own)
+            dst_idx.append(lq.global_rows[own])
+        n_w_max = max(slab_layout(J, P, q).n_w for q in range(P))
+        assert all(slab_layout(J, P, q).n_w == n_w_max for q in range(P))
+        self.gsrc = torch.as_tensor(np.concatenate(src_idx), device=device)
+        self.gdst = torch.as_tensor(np.concatenate(dst_idx), device=device)
+        self.glob = torch.zeros(2 ** J + 1, dtype=dtype, device=device)
+        self.res = torch.zeros(1, dtype=dtype, device=device)
+
+
+# --------------------------------------------------------------------------
+# distributed operators
+# --------------------------------------------------------------------------
+class SlabSystem:
+    """S-hat, K_X and dots over time slabs."""
+
+    def __init__(self, states, comm):
+        self.states = states
+        self.comm = comm
+        self.P = states[0].lay.P
+        self.J = states[0].lay.J
+        self.L0 = states[0].lay.L0
+
+    # W: wavelet X -> nodal rows in U[1 : 1 + n_out]
+    def synthesis(self, X):
+        J, L0, P = self.J, self.L0, self.P
+        for st, x in zip(self.states, X):
+            st.bufs["X"] = x
+            st.CN[0].copy_(x[0:2])
+            for j in range(1, L0 + 1):
+                nc = 2 ** (j - 1) + 1
+                st.k.syn_stage(j, st.CN[j - 1], 0, x[nc:2 ** j + 1], 0, st.CN[j], 0, 2 ** j + 1)
+        for j in range(L0 + 1, J + 1):
+            self.comm.exchange(self.states, lambda lay, j=j: syn_plan(lay, j))
+            n_c = 2 ** (j - 1) // P
+            for st, x in zip(self.states, X):
+                lay = st.lay
+                c0 = lay.p * n_c
+                cin = st.CN[L0][lay.p:lay.p + 2] if j == L0 + 1 else \
+                    st.bufs[_syn_buf(j - 1, J)][1:n_c + 2]
+                off, n = lay.block[j]
+                D = st.bufs["D"]
+                if lay.p == 0:
+                    D[0].zero_()
+                D[1:1 + n].copy_(x[off:off + n])
+                out = st.bufs[_syn_buf(j, J)][1:]
+                st.k.syn_stage(j, cin, c0, D[:n + 1], c0 - 1, out, 2 * c0,
+                               2 * n_c + (1 if lay.last else 0))
+
+    # W^T: nodal rows in Xa[1 : 1 + n_out] -> wavelet Y
+    def analysis(self, Y):
+        J, L0, P = self.J, self.L0, self.P
+        H = self.states[0].lay.H
+        self.comm.exchange(self.states, lambda lay: edge_plan(lay, "Xa", H))
+        for j in range(J, L0, -1):
+            n_c = 2 ** (j - 1) // P
+            for st, y in zip(self.states, Y):
+                lay = st.lay
+                c0 = lay.p * n_c
+                xin = st.bufs[_ana_buf(j, J)][:2 * n_c + 2]
+                cout = st.bufs[_ana_buf(j - 1, J)][1:]
+                off, n = lay.block[j]
+                st.k.ana_stage(j, xin, 2 * c0 - 1, cout, c0, n_c + (1 if lay.last else 0),
+                               y[off:off + n], c0, n_c)
+            if j > L0 + 1:
+                buf = _ana_buf(j - 1, J)
+                self.comm.exchange(self.states, lambda lay, b=buf, n=n_c: edge_plan(lay, b, n))
+        # level-L0 nodes: rank p holds node p (and the last rank node P)
+        buf = _ana_buf(L0, J)
+        gathered = self.comm.allgather(self.states, [st.bufs[buf][1:3] for st in self.states])
+        for st, y, g in zip(self.states, Y, gathered):
+            cn = st.CN[L0]
+            cn[:P].copy_(g[:, 0])
+            cn[P].copy_(g[P - 1, 1])
+            for j in range(L0, 0, -1):
+                nc = 2 ** (j - 1) + 1
+                dst_c = y[0:2] if j == 1 else st.CN[j - 1]
+                st.k.ana_stage(j, st.CN[j], 0, dst_c, 0, nc, y[nc:2 ** j + 1], 0, 2 ** (j - 1))
+            if L0 == 0:
+                y[0:2].copy_(cn[0:2])
+
+    def schur(self, X, Y):
+        """Y = S-hat X (system.py:116-147, 182-187), time-slab distributed."""
+        self.synthesis(X)
+        H = self.states[0].lay.H
+        self.comm.exchange(self.states, lambda lay: edge_plan(lay, "U", H))
+        for st in self.states:
+            lay = st.lay
+            n = lay.n_out
+            st.k.bside_rows(st.bufs["U"], lay.p * H - 1, st.T12[:n], st.T12[n:], lay.p * H, n,
+                            st.E0)
+            st.k.mg_rows_dev(st.ops_zero, st.T12, st.G12)
+            st.k.bt_rows(st.G12[:n], st.G12[n:], st.E0, st.bufs["Xa"][1:1 + n])
+        self.analysis(Y)
+
+    def kx(self, X, Y):
+        """Y = K_X X (system.py:242-276): row-local, no communication."""
+        for st, x, y in zip(self.states, X, Y):
+            st.k.mg_rows_dev(st.ops_kx, x, y)
+            st.k.spatial(1, y, st.mid)
+            st.k.mg_rows_dev(st.ops_kx, st.mid, y)
+
+    def dot(self, X, Y):
+        """Inner product with the reference's fixed tree over the per-row
+        partials in GLOBAL row order (solver.py:111-129) -- identical for
+        every number of ranks."""
+        contrib = []
+        for st, x, y in zip(self.states, X, Y):
+            st.k.row_partials(x, y, st.part)
+            contrib.append(st.part * st.owned)
+        gathered = self.comm.allgather(self.states, contrib)
+        vals = []
+        for st, g in zip(self.states, gathered):
+            st.glob[st.gdst] = g.reshape(-1)[st.gsrc]
+            st.k.tree_sum(st.glob, st.glob.numel(), st.res)
+            vals.append(float(st.res.item()))
+        if len(set(vals)) != 1:
+            raise RuntimeError("ranks disagree on an inner product")
+        return vals[0]
+
+    def axpy(self, a, X, Y):
+        for st, x, y in zip(self.states, X, Y):
+            st.k.axpy(a, x, y)
+
+    def xpay(self, a, X, Y):
+        for st, x, y in zip(self.states, X, Y):
+            st.k.xpay(a, x, y)
+
+
+# --------------------------------------------------------------------------
+# PCG (solver.py:181-263) over time slabs
+# --------------------------------------------------------------------------
+@dataclass
+class SlabPCGResult:
+    iterations: int
+    residual_norms: list
+    alphas: list = field(default_factory=list)
+    betas: list = field(default_factory=list)
+    seconds: float = 0.0
+
+
+def pcg(system: SlabSystem, F, W, epsilon=0.0, rtol=0.0, max_iterations=200,
+        recompute_every=50):
+    """F, W: lists (one per local state) of wavelet-local arrays; W is
+    overwritten with the solution.  Same stopping rule as `api.pcg`."""
+    import torch
+    if not (epsilon > 0) and not (rtol > 0):
+        raise ValueError("tolerance must be positive")
+    t0 = time.perf_counter()
+    R = [f.clone() for f in F]
+    Z = [torch.empty_like(f) for f in F]
+    Pv = [torch.empty_like(f) for f in F]
+    Q = [torch.empty_like(f) for f in F]
+    for w in W:
+        w.zero_()
+    if system.dot(F, F) == 0.0:
+        return SlabPCGResult(0, [0.0])
+    system.kx(R, Z)
+    rho = system.dot(R, Z)
+    hist = [math.sqrt(max(rho, 0.0))]
+    eps = rtol * hist[0] if rtol > 0 else epsilon
+    if rho <= eps ** 2:
+        return SlabPCGResult(0, hist, seconds=time.perf_counter() - t0)
+    for p_, z in zip(Pv, Z):
+        p_.copy_(z)
+    alphas, betas = [], []
+    for it in range(1, max_iterations + 1):
+        system.schur(Pv, Q)
+        pq = system.dot(Pv, Q)
+        if not pq > 0:
+            raise RuntimeError(f"operator lost positive definiteness (p^T S p = {pq:g})")
+        alpha = rho / pq
+        system.axpy(alpha, Pv, W)
+        if it % recompute_every == 0:
+            system.schur(W, Z)
+            for r, f, z in zip(R, F, Z):
+                r.copy_(f)
+            system.axpy(-1.0, Z, R)
+        else:
+            system.axpy(-alpha, Q, R)
+        system.kx(R, Z)
+        rho_new = system.dot(R, Z)
+        beta = rho_new / rho
+        alphas.append(alpha)
+        betas.append(beta)
+        rho = rho_new
+        hist.append(math.sqrt(max(rho, 0.0)))
+        if rho <= eps ** 2:
+            return SlabPCGResult(it, hist, alphas, betas, time.perf_counter() - t0)
+        system.xpay(beta, Z, Pv)
+    from ._lib import IterationLimitError
+    raise IterationLimitError(f"PCG did not reach tolerance {eps:g} within {max_iterations} "
+                              "iterations", hist)
+
+
+# --------------------------------------------------------------------------
+# the CUDA kernel provider and helpers
+# --------------------------------------------------------------------------
+class CudaKernels:
+    """Local kernels of one rank: a kernel-only hwg context on its GPU."""
+
+    def __init__(self, d, J, K, alpha=0.3, vcycles=2, smooth=3, device=0, rows_max=0, D=None,
+                 c=0.0):
+        from .device import GpuContext
+        self.ctx = GpuContext(d, J, K, alpha, vcycles, smooth, D, c, device, rows_max=rows_max)
+        ctx = self.ctx
+        self.syn_stage = ctx.syn_stage
+        self.ana_stage = ctx.ana_stage
+        self.bside_rows = ctx.bside_rows
+        self.bt_rows = ctx.bt_rows
+        self.mg_rows_dev = ctx.mg_rows_dev
+        self.row_partials = ctx.row_partials
+        self.tree_sum = ctx.tree_sum
+        self.axpy = ctx.axpy
+        self.xpay = ctx.xpay
+        self.spatial = ctx.spatial
+
+
+def make_states(d, J, K, P, ranks, device_of, alpha=0.3, vcycles=2, smooth=3):
+    """RankStates (CUDA kernels) for the given ranks of a P-rank slab run."""
+    import torch
+    states = []
+    n_x = (2 ** K - 1) ** d
+    for p in ranks:
+        lay = slab_layout(J, P, p)
+        dev = device_of(p)
+        rows_max = max(2 * lay.n_out, lay.n_w, 2 ** J // P + 2) + 2
+        kern = CudaKernels(d, J, K, alpha, vcycles, smooth, dev.index or 0, rows_max=rows_max)
+        states.append(RankState(lay, kern, n_x, dev, torch.float64))
+    return states
+
+
+def scatter_wavelet(X, lay: RankLayout):
+    """Local wavelet rows of rank `lay.p` from a global (N_t, N_x) array."""
+    import torch
+    idx = torch.as_tensor(lay.global_rows, device=X.device) if hasattr(X, "device") else lay.global_rows
+    return X[idx]
+
+
+def gather_wavelet(parts, layouts, out):
+    """Global array from the ranks' local wavelet rows (owned rows only)."""
+    import torch
+    for x, lay in zip(parts, layouts):
+        own = np.nonzero(lay.owned)[0]
+        if hasattr(out, "device"):
+            out[torch.as_tensor(lay.global_rows[own], device=out.device)] = \
+                x[torch.as_tensor(own, device=x.device)]
+        else:
+            out[lay.global_rows[own]] = x[own]
+    return out

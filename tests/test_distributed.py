@@ -1,0 +1,146 @@
+"""Time-slab distribution: layout properties, the SPMD
+orchestration against the CPU oracle (bit-for-bit) with simulated ranks and
+with a real 2-rank gloo process group, and (GPU) P virtual ranks on one
+device against the single-GPU solver."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2009_08875_b200 import distributed as D
+from paper_2009_08875_b200 import inputs
+
+
+@pytest.mark.parametrize("J,P", [(3, 1), (3, 2), (3, 4), (4, 8), (8, 4), (10, 8)])
+def test_layout_partitions_rows(J, P):
+    n_t = 2 ** J + 1
+    owned_rows = []
+    for p in range(P):
+        lay = D.slab_layout(J, P, p)
+        assert lay.n_w == P + lay.H
+        assert len(lay.global_rows) == lay.n_w
+        owned_rows.extend(lay.global_rows[lay.owned].tolist())
+        assert set(range(P + 1)) <= set(lay.global_rows.tolist())     # replicated coarse rows
+        for j, (off, n) in lay.block.items():
+            g = lay.global_rows[off:off + n]
+            assert np.all(lay.level_of[off:off + n] == j)
+            # wavelets centred in the slab [p/P, (p+1)/P)
+            k = g - 2 ** (j - 1) - 1
+            centre = (2 * k + 1) / 2 ** j
+            assert np.all((centre >= p / P) & (centre < (p + 1) / P))
+    assert sorted(owned_rows) == list(range(n_t))
+
+
+def test_layout_rejects_bad_P():
+    with pytest.raises(ValueError):
+        D.slab_layout(4, 3, 0)
+    with pytest.raises(ValueError):
+        D.slab_layout(3, 8, 0)
+
+
+def _oracle_case(d, J, K, dist="uniform"):
+    from oracle import heatwave_oracle as O
+    system = O.assemble(d, J, K)
+    n_t, n_x = system.shape
+    u0 = inputs.u0_sines if dist == "uniform" else inputs.u0_modes()
+    f = system.rhs(inputs.forcing(dist, n_t, n_x), u0)
+    eps = 1e-6 * np.sqrt(O.dot(f, system.kx(f)))
+    ref = O.pcg(system, f, eps)
+    return O, system, f, eps, ref
+
+
+def _run_slabs(system, f, eps, P, comm, ranks):
+    from slab_numpy import NumpyKernels
+    n_x = system.shape[1]
+    J = system.J
+    states = [D.RankState(D.slab_layout(J, P, p), NumpyKernels(system), n_x, "cpu")
+              for p in ranks]
+    ft = torch.from_numpy(f)
+    F = [D.scatter_wavelet(ft, st.lay).clone() for st in states]
+    W = [torch.zeros_like(x) for x in F]
+    res = D.pcg(D.SlabSystem(states, comm), F, W, epsilon=eps)
+    return states, W, res
+
+
+@pytest.mark.parametrize("d,J,K,P", [(2, 4, 4, 2), (2, 4, 4, 4), (2, 4, 4, 8), (1, 6, 6, 4),
+                                     (2, 3, 5, 2)])
+def test_simulated_ranks_match_oracle_bitwise(d, J, K, P):
+    O, system, f, eps, ref = _oracle_case(d, J, K, "uniform" if d == 2 else "normal")
+    states, W, res = _run_slabs(system, f, eps, P, D.SimComm(P), range(P))
+    assert res.iterations == ref.iterations
+    assert res.residual_norms == ref.residual_norms
+    w = D.gather_wavelet([x.numpy() for x in W], [st.lay for st in states], np.zeros_like(f))
+    assert np.array_equal(w, ref.w)
+    # replicated coarse rows are identical on every rank
+    for st, x in zip(states, W):
+        assert np.array_equal(x[:P + 1].numpy(), ref.w[:P + 1])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, outdir, d, J, K):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        O, system, f, eps, ref = _oracle_case(d, J, K)
+        states, W, res = _run_slabs(system, f, eps, world, D.TorchComm(), [rank])
+        np.save(os.path.join(outdir, f"w{rank}.npy"), W[0].numpy())
+        np.save(os.path.join(outdir, f"its{rank}.npy"), np.array([res.iterations]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_two_ranks_match_oracle_bitwise(world):
+    d, J, K = 2, 4, 4
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as tmp:
+        torch.multiprocessing.spawn(_gloo_worker, args=(world, port, tmp, d, J, K), nprocs=world,
+                                    join=True)
+        O, system, f, eps, ref = _oracle_case(d, J, K)
+        parts = [np.load(os.path.join(tmp, f"w{r}.npy")) for r in range(world)]
+        its = [int(np.load(os.path.join(tmp, f"its{r}.npy"))[0]) for r in range(world)]
+    assert its == [ref.iterations] * world
+    lays = [D.slab_layout(J, world, p) for p in range(world)]
+    w = D.gather_wavelet(parts, lays, np.zeros_like(f))
+    assert np.array_equal(w, ref.w)
+
+
+# ---------------------------------------------------------------------------
+# GPU: P virtual ranks on one device vs the single-GPU solver
+# ---------------------------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,J,K,Ps", [(2, 4, 4, (1, 2, 4, 8)), (2, 3, 6, (1, 2, 4)),
+                                      (1, 6, 6, (2, 4)), (2, 8, 8, (1, 4))])
+def test_gpu_virtual_ranks_match_single_gpu(d, J, K, Ps):
+    import paper_2009_08875_b200 as hw
+    dist_name = "uniform" if d == 2 else "normal"
+    u0 = inputs.u0_sines if d == 2 else inputs.u0_modes()
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** d
+    F = inputs.forcing(dist_name, n_t, n_x)
+    asm = hw.assemble_system(hw.ProblemData(D=np.eye(d), c=0.0, u0=u0), J, K, hw.SolveConfig(),
+                             forcing=F, host_rhs=False)
+    f = asm.rhs.f_hat.array
+    w1 = torch.empty_like(f)
+    stats, rc = asm.ctx.pcg(f, w1, 0.0, 1e-6)
+    assert rc == 0
+    dev = torch.device("cuda", 0)
+    for P in Ps:
+        states = D.make_states(d, J, K, P, range(P), lambda p: dev)
+        Fl = [D.scatter_wavelet(f, st.lay).clone() for st in states]
+        Wl = [torch.zeros_like(x) for x in Fl]
+        res = D.pcg(D.SlabSystem(states, D.SimComm(P)), Fl, Wl, rtol=1e-6)
+        assert res.iterations == stats["iterations"], P
+        w = D.gather_wavelet(Wl, [st.lay for st in states], torch.zeros_like(f))
+        assert torch.equal(w, w1), (P, float((w - w1).abs().max()))
