@@ -14,9 +14,11 @@ BASELINE config's shape and distribution (no dataset exists).
 oracle/ (C + OpenMP over all host cores; the reference itself is Python +
 numba and cannot travel to the GPU box) -- one PCG iteration per step.
 
-N > 1 (torchrun): every rank solves its own replica of the workload
-("weak" scaling, no collective on the data path; time-slab sharding across
-GPUs is not built yet).
+N > 1 (torchrun): the workload is partitioned in time slabs across the N
+GPUs (paper_2009_08875_b200/distributed.py, SURVEY §8e design (a)): NCCL
+halo rows for the temporal bands and wavelet stages, an allgather of the
+coarse wavelet levels and of the dot partials; "scaling": "strong" (total
+work fixed).  --slab runs the same distributed path at N = 1.
 """
 
 from __future__ import annotations
@@ -216,9 +218,6 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
     d, J, K, dist_name, u0, n_t, n_x = workload(args.config)
     N = n_t * n_x
     problem = hw.ProblemData(D=np.eye(d), c=0.0, u0=u0)
@@ -351,6 +350,118 @@ def run_ours(args):
     return 0
 
 
+def run_slab(args):
+    """Time-slab distributed solve over N GPUs (strong scaling)."""
+    import torch
+    import torch.distributed as tdist
+    from paper_2009_08875_b200 import distributed as D
+    from paper_2009_08875_b200 import discretization as disc
+
+    rank, world, local = dist_env()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tdist.init_process_group("nccl", device_id=dev)
+    d, J, K, dist_name, u0, n_t, n_x = workload(args.config)
+    N = n_t * n_x
+    states = D.make_states(d, J, K, world, [rank], lambda p: dev)
+    system = D.SlabSystem(states, D.TorchComm())
+    st = states[0]
+    lay = st.lay
+
+    def frows(a, b):
+        return torch.from_numpy(inputs.forcing_rows(dist_name, n_t, n_x, a, b)).to(dev)
+
+    u0p = torch.from_numpy(disc.project_initial(disc.FineMesh(d, K), u0)).to(dev)
+    F = D.rhs(system, frows, u0p)
+    W = [torch.empty_like(F[0])]
+
+    def solve():
+        return D.pcg(system, F, W, rtol=1e-6).iterations
+
+    for _ in range(args.warmup):
+        solve()
+    ctx = st.k.ctx
+    torch.cuda.synchronize()
+    tdist.barrier()
+    launches0 = ctx.launches
+    ctx.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        tdist.barrier()
+        e0.record()
+        its_list = [solve() for _ in range(args.steps)]
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    launches = ctx.launches - launches0
+    t = torch.tensor([ms], device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_its = sum(its_list)
+    value = N * total_its / (ms_max / 1e3)
+
+    # e2e: pinned host f-hat rows in, u rows out, every step
+    fh = [torch.empty(F[0].shape, dtype=torch.float64, pin_memory=True)]
+    fh[0].copy_(F[0])
+    uh = [torch.empty((lay.n_out, n_x), dtype=torch.float64, pin_memory=True)]
+    D.solve_host(system, fh, uh)
+    tdist.barrier()
+    t0 = time.perf_counter()
+    e2e_its = 0
+    for _ in range(args.steps):
+        e2e_its += D.solve_host(system, fh, uh).iterations
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+
+    peak, peak_src = measured_peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dbytes, dn) = dom
+    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    model = model_bytes_per_iteration(d, J, K)
+    it_s = (ms_max / 1e3) / total_its
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE recipe, blockwise-seeded forcing rows)",
+            "config": {"workload": f"cfg{args.config}: {d}D heat, J={J} (N_t={n_t}), "
+                                   f"K={K} (N_x={n_x}), PCG to rtol 1e-6",
+                       "dofs": N, "iterations_per_solve": its_list[0],
+                       "parallelism": f"time slabs x{world} (NCCL halos + allgather)",
+                       "l2": "inputs larger than L2"},
+            "time_to_solve_s": ms_max / 1e3 / args.steps,
+            "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "launches": dn, "bytes_per_launch": dbytes / max(dn, 1),
+                         "peak_source": peak_src, "rank": 0},
+            "roofline_model": {"bytes_per_iteration": model, "s_per_iteration": it_s,
+                               "achieved_GBs": model / it_s / 1e9,
+                               "frac": model / it_s / 1e9 / (peak * world),
+                               "source": "SURVEY.md §8d streaming model, aggregate over GPUs"},
+            "kernel_classes_ms": {k: v[0] for k, v in prof.items()},
+            "e2e": {"value": N * e2e_its / e2e_s, "unit": UNIT, "h2d_bytes_per_step":
+                    8 * n_x * sum(D.slab_layout(J, world, q).n_w for q in range(world)),
+                    "d2h_bytes_per_step": 8 * N, "time_to_solve_s": e2e_s / args.steps},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,9 +471,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-iterations", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="time-slab path even at N = 1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.slab or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_slab(args)
     return run_ours(args)
 
 

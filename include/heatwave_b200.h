@@ -219,6 +219,13 @@ int hwg_bside_rows(hwg_ctx *ctx, const double *U, int64_t u0, int64_t nu, double
 int hwg_bt_rows(hwg_ctx *ctx, const double *G1, const double *G2, const double *E0, double *out,
                 int64_t rows, void *stream);
 
+/* Temporal factor on a row range: Y[c - r0] = sum_k B[c,k] X[k - x0] for
+ * c in [r0, r0 + nr) (temporal_apply, _kernels.py:37-52).  band: 0 M_t,
+ * 1 A_t, 2 L, 3 L^T, 4 T, 5 T^T, 6 N, 7 N^T (temporal.py:82-144; T and N
+ * have 2*2^J test rows).  X must hold every row the band touches. */
+int hwg_temporal_rows(hwg_ctx *ctx, int band, const double *X, int64_t x0, double *Y, int64_t r0,
+                      int64_t nr, void *stream);
+
 /* Batched V-cycles with a DEVICE array of per-row operator ids. */
 int hwg_mg_rows_dev(hwg_ctx *ctx, const int32_t *ops, const double *B, double *X, int64_t rows,
                     void *stream);

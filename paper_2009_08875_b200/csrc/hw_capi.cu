@@ -847,4 +847,17 @@ int hwg_xpay(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *
     return HWG_OK;
 }
 
+int hwg_temporal_rows(hwg_ctx *c, int band, const double *X, int64_t x0, double *Y, int64_t r0,
+                      int64_t nr, void *stream)
+{
+    if (!c || !X || !Y || nr < 0 || r0 < 0) return fail(HWG_EINVAL, "bad argument");
+    const DevBand *bands[8] = {&c->Mt, &c->At, &c->L, &c->LT, &c->T, &c->TT, &c->Nn, &c->NT};
+    if (band < 0 || band > 7) return fail(HWG_EINVAL, "unknown temporal band");
+    const int64_t rows = (band == 4 || band == 6) ? 2 * (c->nt - 1) : c->nt;
+    if (r0 + nr > rows) return fail(HWG_EINVAL, "row range outside the band");
+    CK(launch_temporal_rows(bands[band]->view(), X, x0, Y, r0, nr, c->nx, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
 }  // extern "C"

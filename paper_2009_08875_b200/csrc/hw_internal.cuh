@@ -93,6 +93,8 @@ cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *
                                int64_t r0, int64_t nr, int64_t nt, cudaStream_t st);
 cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
                        cudaStream_t st);
+cudaError_t launch_temporal_rows(TCsr B, const double *X, int64_t x0, double *Y, int64_t r0,
+                                 int64_t nr, int64_t nx, cudaStream_t st);
 
 // ---- hw_vec.cu -----------------------------------------------------------
 cudaError_t launch_dot(const double *X, const double *Y, int64_t rows, int64_t nx, double *part,

@@ -184,6 +184,24 @@ __device__ __forceinline__ double tcsr_row(const TCsr &B, int64_t c, const doubl
     return acc;
 }
 
+// Y[c - r0] = sum_k B[c,k] X[k - x0], c in [r0, r0 + nr)
+__global__ void temporal_rows(TCsr B, const double *__restrict__ X, int64_t x0,
+                              double *__restrict__ Y, int64_t r0, int64_t nr, int64_t nx)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    for (int64_t rr = blockIdx.y; rr < nr; rr += gridDim.y) {
+        const int64_t c = r0 + rr;
+        const int k0 = B.ip[c], k1 = B.ip[c + 1];
+        double acc = 0.0;
+        for (int k = k0; k < k1; ++k) {
+            const double v = mul_rn(B.v[k], X[((int64_t)B.ix[k] - x0) * nx + i]);
+            acc = (k == k0) ? v : add_rn(acc, v);
+        }
+        Y[rr * nx + i] = acc;
+    }
+}
+
 __global__ void temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -253,6 +271,15 @@ cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t 
     dim3 grid((unsigned)((nx + 255) / 256),
               (unsigned)(rows < 65535 ? (rows < 1 ? 1 : rows) : 65535));
     temporal_bands<<<grid, 256, 0, st>>>(o1, o2, rows, nx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_temporal_rows(TCsr B, const double *X, int64_t x0, double *Y, int64_t r0,
+                                 int64_t nr, int64_t nx, cudaStream_t st)
+{
+    if (nr <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nr < 65535 ? nr : 65535));
+    temporal_rows<<<grid, 256, 0, st>>>(B, X, x0, Y, r0, nr, nx);
     return cudaGetLastError();
 }
 

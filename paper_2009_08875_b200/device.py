@@ -132,6 +132,12 @@ class GpuContext:
                                         ptr(E0) if E0 is not None else None, ptr(out),
                                         out.shape[0], self.stream()))
 
+    BANDS = {"Mt": 0, "At": 1, "L": 2, "LT": 3, "T": 4, "TT": 5, "N": 6, "NT": 7}
+
+    def temporal_rows(self, band, X, x0, Y, r0, nr):
+        _lib.check(self.lib.hwg_temporal_rows(self.handle, self.BANDS[band], ptr(X), x0, ptr(Y),
+                                              r0, nr, self.stream()))
+
     def mg_rows_dev(self, ops, B, X):
         _lib.check(self.lib.hwg_mg_rows_dev(self.handle, ptr(ops), ptr(B), ptr(X), B.shape[0],
                                             self.stream()))

@@ -445,6 +445,7 @@ class CudaKernels:
         self.axpy = ctx.axpy
         self.xpay = ctx.xpay
         self.spatial = ctx.spatial
+        self.temporal_rows = ctx.temporal_rows
 
 
 def make_states(d, J, K, P, ranks, device_of, alpha=0.3, vcycles=2, smooth=3):
@@ -479,3 +480,66 @@ def gather_wavelet(parts, layouts, out):
         else:
             out[lay.global_rows[own]] = x[own]
     return out
+
+
+# --------------------------------------------------------------------------
+# right-hand side over time slabs (system.py:295-324)
+# --------------------------------------------------------------------------
+def rhs(system: SlabSystem, forcing_rows, u0proj):
+    """Local slices of f-hat = W^T( B^T K_Y (N (x) M_x) F + e_0 (x) <u0, phi> ).
+
+    forcing_rows(r0, r1) -> nodal forcing rows [r0, r1) as a tensor on the
+    rank's device (the blockwise-seeded generator makes them independent of
+    P); u0proj: the N_x moments <u0, phi_i> (used by rank 0 only).  Returns
+    one wavelet-local array per state.  Each rank assembles the test-space
+    load of the time elements touching its slab (one halo element), applies
+    K_Y = O^-1 (x) K_x (O = I) row-locally, B^T on its nodal rows and the
+    distributed W^T."""
+    import torch
+    J, P = system.J, system.P
+    nt = 2 ** J + 1
+    G = []
+    for st in system.states:
+        lay = st.lay
+        H = lay.H
+        e0, e1 = max(lay.p * H - 1, 0), min(lay.p * H + H, nt - 1)     # time elements
+        Fr = forcing_rows(e0, e1 + 1)                                   # nodes e0..e1
+        MxF = torch.empty_like(Fr)
+        st.k.spatial(0, Fr, MxF)
+        y = torch.empty((2 * (e1 - e0), Fr.shape[1]), dtype=Fr.dtype, device=Fr.device)
+        st.k.temporal_rows("N", MxF, e0, y, 2 * e0, 2 * (e1 - e0))
+        ky = torch.empty_like(y)
+        st.k.mg_rows_dev(torch.zeros(y.shape[0], dtype=torch.int32, device=y.device), y, ky)
+        n = lay.n_out
+        w1 = torch.empty((n, Fr.shape[1]), dtype=Fr.dtype, device=Fr.device)
+        w2 = torch.empty_like(w1)
+        st.k.temporal_rows("TT", ky, 2 * e0, w1, lay.p * H, n)
+        st.k.temporal_rows("NT", ky, 2 * e0, w2, lay.p * H, n)
+        st.k.bt_rows(w1, w2, None, st.bufs["Xa"][1:1 + n])
+        G.append(torch.empty((lay.n_w, Fr.shape[1]), dtype=Fr.dtype, device=Fr.device))
+    system.analysis(G)
+    U = []
+    for st in system.states:
+        xa = st.bufs["Xa"]
+        xa.zero_()
+        if st.lay.p == 0 and u0proj is not None:
+            xa[1].copy_(u0proj)
+        U.append(torch.empty_like(G[len(U)]))
+    system.analysis(U)
+    return [g + u for g, u in zip(G, U)]
+
+
+def solve_host(system: SlabSystem, f_host, u_host, rtol=1e-6, epsilon=0.0, max_iterations=200):
+    """End-to-end slab solve with host buffers (bench e2e leg): copies this
+    rank's f-hat rows in, runs PCG, forms its nodal rows of u = W w and
+    copies them out.  f_host / u_host: lists of pinned host tensors per
+    state ((n_w, N_x) and (n_out, N_x))."""
+    import torch
+    F = [fh.to(st.bufs["U"].device, non_blocking=True) for fh, st in zip(f_host, system.states)]
+    W = [torch.empty_like(f) for f in F]
+    res = pcg(system, F, W, epsilon=epsilon, rtol=rtol, max_iterations=max_iterations)
+    system.synthesis(W)
+    for st, uh in zip(system.states, u_host):
+        uh.copy_(st.bufs["U"][1:1 + st.lay.n_out], non_blocking=True)
+    torch.cuda.synchronize()
+    return res

@@ -107,3 +107,16 @@ class NumpyKernels:
 
     def xpay(self, a, X, Y):
         O.xpay(a, np.ascontiguousarray(_np(X)), _np(Y))
+
+    # --- temporal factor on a row range (distributed RHS) --------------------
+    def temporal_rows(self, band, X, x0, Y, r0, nr):
+        s = self.s
+        B = {"Mt": s.Mt, "At": s.At, "L": s.L, "LT": s.LT, "T": s.T, "TT": s.T.T,
+             "N": s.N, "NT": s.N.T}[band]
+        X = _np(X)
+        Xg = np.zeros((B.shape[1], self.nx))
+        for r in range(X.shape[0]):
+            if 0 <= x0 + r < B.shape[1]:
+                Xg[x0 + r] = X[r]
+        out = O.temporal(B, Xg, np.empty((B.shape[0], self.nx)))
+        _np(Y)[:nr] = out[r0:r0 + nr]

@@ -144,3 +144,41 @@ def test_gpu_virtual_ranks_match_single_gpu(d, J, K, Ps):
         assert res.iterations == stats["iterations"], P
         w = D.gather_wavelet(Wl, [st.lay for st in states], torch.zeros_like(f))
         assert torch.equal(w, w1), (P, float((w - w1).abs().max()))
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_simulated_rhs_matches_oracle_bitwise(P):
+    from oracle import heatwave_oracle as O
+    from slab_numpy import NumpyKernels
+    d, J, K = 2, 4, 4
+    system = O.assemble(d, J, K)
+    n_t, n_x = system.shape
+    F = inputs.forcing("uniform", n_t, n_x)
+    want = system.rhs(F, inputs.u0_sines)
+    u0p = torch.from_numpy(O.project_initial(system.finest, inputs.u0_sines))
+    states = [D.RankState(D.slab_layout(J, P, p), NumpyKernels(system), n_x, "cpu")
+              for p in range(P)]
+    sysd = D.SlabSystem(states, D.SimComm(P))
+    parts = D.rhs(sysd, lambda a, b: torch.from_numpy(F[a:b].copy()), u0p)
+    got = D.gather_wavelet([x.numpy() for x in parts], [st.lay for st in states], np.zeros_like(want))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,J,K,P", [(2, 4, 4, 4), (2, 8, 8, 4), (1, 6, 6, 2)])
+def test_gpu_virtual_ranks_rhs(d, J, K, P):
+    import paper_2009_08875_b200 as hw
+    from paper_2009_08875_b200 import discretization as disc
+    dist_name = "uniform" if d == 2 else "normal"
+    u0 = inputs.u0_sines if d == 2 else inputs.u0_modes()
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** d
+    F = inputs.forcing(dist_name, n_t, n_x)
+    asm = hw.assemble_system(hw.ProblemData(D=np.eye(d), c=0.0, u0=u0), J, K, hw.SolveConfig(),
+                             forcing=F, host_rhs=False)
+    dev = torch.device("cuda", 0)
+    states = D.make_states(d, J, K, P, range(P), lambda p: dev)
+    u0p = torch.from_numpy(disc.project_initial(disc.FineMesh(d, K), u0)).to(dev)
+    Ft = torch.from_numpy(F).to(dev)
+    parts = D.rhs(D.SlabSystem(states, D.SimComm(P)), lambda a, b: Ft[a:b], u0p)
+    got = D.gather_wavelet(parts, [st.lay for st in states], torch.zeros_like(asm.rhs.f_hat.array))
+    assert torch.equal(got, asm.rhs.f_hat.array)
