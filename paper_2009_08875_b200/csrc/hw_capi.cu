@@ -47,6 +47,7 @@ static int fail(int code, const std::string &msg)
 struct DevBand {           // a temporal factor in CSR on the device
     int32_t *ip = nullptr, *ix = nullptr;
     double *v = nullptr;
+    double *tri = nullptr;   // dense (lo, mid, hi) per row (tridiagonal factors)
     TCsr view() const { return TCsr{ip, ix, v}; }
 };
 
@@ -180,6 +181,16 @@ static int make_band(hwg_ctx *c, DevBand *b, const std::vector<std::vector<std::
     TRY(upload(c, &b->ip, ip));
     TRY(upload(c, &b->ix, ix));
     TRY(upload(c, &b->v, v));
+    // dense triples when every entry lies within one row of the diagonal
+    std::vector<double> tri(3 * rows.size(), 0.0);
+    bool banded = true;
+    for (size_t r = 0; r < rows.size(); ++r)
+        for (auto &e : rows[r]) {
+            const long d = (long)e.first - (long)r;
+            if (d < -1 || d > 1) banded = false;
+            else tri[3 * r + (d + 1)] = e.second;
+        }
+    if (banded) TRY(upload(c, &b->tri, tri));
     return HWG_OK;
 }
 
@@ -356,7 +367,7 @@ static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
     // t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU (one pass over U); the
     // first row of MxU is kept for the trace term
     CK(launch_bside_fused(c->U, 0, c->T12, c->T12 + N, c->MxU, c->grid, c->SM, c->SA,
-                          c->At.view(), c->LT.view(), c->Mt.view(), c->L.view(), 0, nt, nt, st));
+                          Tri4{c->At.tri, c->LT.tri, c->Mt.tri, c->L.tri}, 0, nt, nt, st));
     ++c->launches;
     TRY(mg_apply(c, c->T12, c->G12, 2 * nt, 0, nullptr, st));
     CK(launch_bt_side(c->G12, c->G12 + N, c->MxU, c->U, c->grid, c->SM, c->SA, nt, st));
@@ -789,7 +800,7 @@ int hwg_bside_rows(hwg_ctx *c, const double *U, int64_t u0, int64_t nu, double *
         return fail(HWG_EINVAL, "U does not cover the rows the temporal bands need");
     if (nr == 0) return HWG_OK;
     CK(launch_bside_fused(U, u0, T1, T2, r0 == 0 ? E0 : nullptr, c->grid, c->SM, c->SA,
-                          c->At.view(), c->LT.view(), c->Mt.view(), c->L.view(), r0, nr, c->nt,
+                          Tri4{c->At.tri, c->LT.tri, c->Mt.tri, c->L.tri}, r0, nr, c->nt,
                           S(stream)));
     ++c->launches;
     return HWG_OK;

@@ -77,6 +77,9 @@ struct TCsr {              // temporal factor, CSR on the device
     const int32_t *ip, *ix;
     const double *v;
 };
+struct Tri4 {              // dense (lo, mid, hi) rows of A_t, L^T, M_t, L (device)
+    const double *At, *LT, *Mt, *L;
+};
 struct BandOut {           // out = b1 x1 (+ b2 x2)
     TCsr b1, b2;
     const double *x1, *x2;
@@ -89,8 +92,8 @@ cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0,
 cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx,
                                   cudaStream_t st);
 cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *T2, double *E0,
-                               Grid g, Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
-                               int64_t r0, int64_t nr, int64_t nt, cudaStream_t st);
+                               Grid g, Stencil M, Stencil A, Tri4 tri, int64_t r0, int64_t nr,
+                               int64_t nt, cudaStream_t st);
 cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
                        cudaStream_t st);
 cudaError_t launch_temporal_rows(TCsr B, const double *X, int64_t x0, double *Y, int64_t r0,

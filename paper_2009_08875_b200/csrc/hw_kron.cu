@@ -40,38 +40,61 @@ __device__ __forceinline__ Pt point_of(const Grid &g)
     return p;
 }
 
-// y = S x at one point (CSR column order; the diagonal coupling exists in
-// the CSR only where its value is nonzero)
-__device__ __forceinline__ double stencil_pt(const double *__restrict__ x, const Pt &p,
-                                             const Grid &g, const Stencil &s)
-{
-    const int m = g.m;
-    if (g.dim == 1) {
-        const int j = p.j;
-        double acc = mul_rn(s.c0, __ldg(x + j));
-        if (j > 0) acc = add_rn(mul_rn(s.cy, __ldg(x + j - 1)), acc);
-        if (j < m - 1) acc = add_rn(acc, mul_rn(s.cy, __ldg(x + j + 1)));
-        return acc;
-    }
-    const bool diag = s.cd != 0.0;
-    const int i = p.i, j = p.j;
-    const int64_t k = (int64_t)i * m + j;
-    double acc = 0.0;
-    bool first = true;
-    auto add = [&](double v) { acc = first ? v : add_rn(acc, v); first = false; };
-    if (diag && i > 0 && j > 0) add(mul_rn(s.cd, __ldg(x + k - m - 1)));
-    if (i > 0) add(mul_rn(s.cx, __ldg(x + k - m)));
-    if (j > 0) add(mul_rn(s.cy, __ldg(x + k - 1)));
-    add(mul_rn(s.c0, __ldg(x + k)));
-    if (j < m - 1) add(mul_rn(s.cy, __ldg(x + k + 1)));
-    if (i < m - 1) add(mul_rn(s.cx, __ldg(x + k + m)));
-    if (diag && i < m - 1 && j < m - 1) add(mul_rn(s.cd, __ldg(x + k + m + 1)));
-    return acc;
-}
-
 __device__ __forceinline__ int64_t pidx(const Pt &p, const Grid &g)
 {
     return g.dim == 2 ? (int64_t)p.i * g.m + p.j : p.j;
+}
+
+// ---- point stencils with direct (read-only cached) loads -------------------
+// x points at the grid point itself.  The interior path is straight-line
+// (all seven couplings present); boundary points skip absent couplings.
+// Arithmetic in the reference's CSR column order (csr_rows_matvec).
+template <bool DIAG>
+__device__ __forceinline__ double stencil2(const double *__restrict__ x, int i, int j, int m,
+                                           bool interior, const Stencil &s)
+{
+    if (interior) {
+        double acc;
+        if (DIAG) {
+            acc = mul_rn(s.cd, __ldg(x - m - 1));
+            acc = add_rn(acc, mul_rn(s.cx, __ldg(x - m)));
+        } else {
+            acc = mul_rn(s.cx, __ldg(x - m));
+        }
+        acc = add_rn(acc, mul_rn(s.cy, __ldg(x - 1)));
+        acc = add_rn(acc, mul_rn(s.c0, __ldg(x)));
+        acc = add_rn(acc, mul_rn(s.cy, __ldg(x + 1)));
+        acc = add_rn(acc, mul_rn(s.cx, __ldg(x + m)));
+        if (DIAG) acc = add_rn(acc, mul_rn(s.cd, __ldg(x + m + 1)));
+        return acc;
+    }
+    double acc = 0.0;
+    bool first = true;
+    auto add = [&](double v) { acc = first ? v : add_rn(acc, v); first = false; };
+    if (DIAG && i > 0 && j > 0) add(mul_rn(s.cd, __ldg(x - m - 1)));
+    if (i > 0) add(mul_rn(s.cx, __ldg(x - m)));
+    if (j > 0) add(mul_rn(s.cy, __ldg(x - 1)));
+    add(mul_rn(s.c0, __ldg(x)));
+    if (j < m - 1) add(mul_rn(s.cy, __ldg(x + 1)));
+    if (i < m - 1) add(mul_rn(s.cx, __ldg(x + m)));
+    if (DIAG && i < m - 1 && j < m - 1) add(mul_rn(s.cd, __ldg(x + m + 1)));
+    return acc;
+}
+
+__device__ __forceinline__ double stencil1(const double *__restrict__ x, int j, int m,
+                                           const Stencil &s)
+{
+    double acc = mul_rn(s.c0, __ldg(x));
+    if (j > 0) acc = add_rn(mul_rn(s.cy, __ldg(x - 1)), acc);
+    if (j < m - 1) acc = add_rn(acc, mul_rn(s.cy, __ldg(x + 1)));
+    return acc;
+}
+
+template <bool DIAG>
+__device__ __forceinline__ double stencil_at(const double *__restrict__ x, const Pt &p,
+                                             const Grid &g, bool interior, const Stencil &S)
+{
+    return g.dim == 2 ? stencil2<DIAG>(x, p.i, p.j, g.m, interior, S) : stencil1(x, p.j, g.m, S);
 }
 
 static dim3 spatial_grid(const Grid &g, int64_t rows)
@@ -81,7 +104,13 @@ static dim3 spatial_grid(const Grid &g, int64_t rows)
     return dim3((g.m + TX * TY - 1) / (TX * TY), 1, z);
 }
 
+__device__ __forceinline__ bool interior_of(const Pt &p, const Grid &g)
+{
+    return p.i > 0 && p.j > 0 && p.i < g.m - 1 && p.j < g.m - 1;
+}
+
 // YM = M X, YA = A X (either output may be null)
+template <bool DM, bool DA>
 __global__ void __launch_bounds__(TX * TY) stencil_rows(const double *__restrict__ X,
                                                         double *__restrict__ YM,
                                                         double *__restrict__ YA, Grid g,
@@ -89,16 +118,18 @@ __global__ void __launch_bounds__(TX * TY) stencil_rows(const double *__restrict
 {
     const Pt p = point_of(g);
     if (!p.ok) return;
-    const int64_t k = pidx(p, g);
+    const int k = (int)pidx(p, g);
+    const bool in = interior_of(p, g);
     for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) {
-        const double *x = X + r * g.nx;
-        if (YM) YM[r * g.nx + k] = stencil_pt(x, p, g, M);
-        if (YA) YA[r * g.nx + k] = stencil_pt(x, p, g, A);
+        const int64_t o = r * g.nx + k;
+        if (YM) YM[o] = stencil_at<DM>(X + o, p, g, in, M);
+        if (YA) YA[o] = stencil_at<DA>(X + o, p, g, in, A);
     }
 }
 
 // out = M G1 + A G2; row 0 additionally += E0 (the trace term Gamma0 (x) M_x)
 // -- system.py:134,141-142,145
+template <bool DM, bool DA>
 __global__ void __launch_bounds__(TX * TY) bt_side(const double *__restrict__ G1,
                                                    const double *__restrict__ G2,
                                                    const double *__restrict__ E0,
@@ -107,66 +138,68 @@ __global__ void __launch_bounds__(TX * TY) bt_side(const double *__restrict__ G1
 {
     const Pt p = point_of(g);
     if (!p.ok) return;
-    const int64_t k = pidx(p, g);
+    const int k = (int)pidx(p, g);
+    const bool in = interior_of(p, g);
     for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) {
-        double v = add_rn(stencil_pt(G1 + r * g.nx, p, g, M), stencil_pt(G2 + r * g.nx, p, g, A));
+        const int64_t o = r * g.nx + k;
+        double v = add_rn(stencil_at<DM>(G1 + o, p, g, in, M), stencil_at<DA>(G2 + o, p, g, in, A));
         if (r == 0 && E0) v = add_rn(v, E0[k]);
-        out[r * g.nx + k] = v;
+        out[o] = v;
     }
 }
 
-// one CSR row of a temporal factor applied to the values of rows c-1, c, c+1
-// (these factors have no other entries)
-__device__ __forceinline__ double band3(const TCsr &B, int64_t c, double vm, double v0, double vp)
+// a temporal band row as a dense (lo, mid, hi) triple; absent CSR entries
+// are 0 (adding 0 * x leaves the CSR-order sum unchanged up to signed zeros)
+__device__ __forceinline__ double band3(const double *__restrict__ tri, int64_t c, double vm,
+                                        double v0, double vp)
 {
-    const int k0 = B.ip[c], k1 = B.ip[c + 1];
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k) {
-        const int d = B.ix[k] - (int)c;
-        const double x = d < 0 ? vm : (d == 0 ? v0 : vp);
-        acc = (k == k0) ? mul_rn(B.v[k], x) : add_rn(acc, mul_rn(B.v[k], x));
-    }
-    return acc;
+    const double *b = tri + 3 * c;
+    double acc = mul_rn(__ldg(b), vm);
+    acc = add_rn(acc, mul_rn(__ldg(b + 1), v0));
+    return add_rn(acc, mul_rn(__ldg(b + 2), vp));
 }
 
 // B-side, fused: t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU with
-// MxU = M_x U, AxU = A_x U computed on the fly (system.py:119-139).  Each CTA
-// owns a spatial tile and a chunk of temporal rows and slides a 3-row window
-// of (MxU, AxU) in registers, so U is read once and t1, t1' written once.
-// Output rows are the global temporal rows [r0, r0 + nr) (T1/T2 indexed from
-// r0); U holds global rows [u0, ...) including the halo rows the bands touch;
-// nt is the global row count.  E0 (optional) receives M_x U[0].
+// MxU = M_x U, AxU = A_x U computed on the fly (system.py:119-139).  Each
+// thread owns one grid point and a chunk of temporal rows and slides a 3-row
+// window of (MxU, AxU) in registers, so U is read once and t1, t1' written
+// once.  Output rows are the global temporal rows [r0, r0 + nr) (T1/T2
+// indexed from r0); U holds global rows [u0, ...) including the halo rows
+// the bands touch; nt is the global row count.  E0 (optional) receives
+// M_x U[0].
+template <bool DM, bool DA>
 __global__ void __launch_bounds__(TX * TY) bside_fused(const double *__restrict__ U, int64_t u0,
                                                        double *__restrict__ T1,
                                                        double *__restrict__ T2,
                                                        double *__restrict__ E0, Grid g,
-                                                       Stencil M, Stencil A, TCsr At, TCsr LT,
-                                                       TCsr Mt, TCsr Lm, int64_t r0, int64_t nr,
-                                                       int64_t nt, int chunk)
+                                                       Stencil M, Stencil A, Tri4 tri,
+                                                       int64_t r0, int64_t nr, int64_t nt,
+                                                       int chunk)
 {
     const Pt p = point_of(g);
     if (!p.ok) return;
-    const int64_t k = pidx(p, g);
-    auto urow = [&](int64_t c) { return U + (c - u0) * g.nx; };
+    const int k = (int)pidx(p, g);
+    const bool in = interior_of(p, g);
+    const double *Uk = U + k;
+    auto st = [&](int64_t c, double &mv, double &av) {
+        const double *x = Uk + (c - u0) * g.nx;
+        mv = stencil_at<DM>(x, p, g, in, M);
+        av = stencil_at<DA>(x, p, g, in, A);
+    };
     for (int64_t c0 = r0 + (int64_t)blockIdx.z * chunk; c0 < r0 + nr;
          c0 += (int64_t)gridDim.z * chunk) {
         const int64_t c1 = c0 + chunk < r0 + nr ? c0 + chunk : r0 + nr;
         double mm = 0.0, am = 0.0;                     // row c-1
-        if (c0 > 0) {
-            mm = stencil_pt(urow(c0 - 1), p, g, M);
-            am = stencil_pt(urow(c0 - 1), p, g, A);
-        }
-        double m0 = stencil_pt(urow(c0), p, g, M);
-        double a0 = stencil_pt(urow(c0), p, g, A);
+        if (c0 > 0) st(c0 - 1, mm, am);
+        double m0, a0;
+        st(c0, m0, a0);
         if (c0 == 0 && E0) E0[k] = m0;
         for (int64_t c = c0; c < c1; ++c) {
             double mp = 0.0, ap = 0.0;                 // row c+1
-            if (c + 1 < nt) {
-                mp = stencil_pt(urow(c + 1), p, g, M);
-                ap = stencil_pt(urow(c + 1), p, g, A);
-            }
-            T1[(c - r0) * g.nx + k] = add_rn(band3(At, c, mm, m0, mp), band3(LT, c, am, a0, ap));
-            T2[(c - r0) * g.nx + k] = add_rn(band3(Mt, c, am, a0, ap), band3(Lm, c, mm, m0, mp));
+            if (c + 1 < nt) st(c + 1, mp, ap);
+            const int64_t o = (c - r0) * g.nx + k;
+            T1[o] = add_rn(band3(tri.At, c, mm, m0, mp), band3(tri.LT, c, am, a0, ap));
+            T2[o] = add_rn(band3(tri.Mt, c, am, a0, ap), band3(tri.L, c, mm, m0, mp));
             mm = m0; am = a0;
             m0 = mp; a0 = ap;
         }
@@ -237,31 +270,46 @@ static unsigned grid_for(int64_t total, int bs)
 cudaError_t launch_stencil_rows(const double *X, double *YM, double *YA, Grid g, Stencil M,
                                 Stencil A, int64_t rows, cudaStream_t st)
 {
-    stencil_rows<<<spatial_grid(g, rows), dim3(TX, TY), 0, st>>>(X, YM, YA, g, M, A, rows);
+    const bool dm = M.cd != 0.0, da = A.cd != 0.0;
+    const dim3 grid = spatial_grid(g, rows), block(TX, TY);
+    if (dm && da) stencil_rows<true, true><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
+    else if (dm) stencil_rows<true, false><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
+    else if (da) stencil_rows<false, true><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
+    else stencil_rows<false, false><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0, double *out,
                            Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st)
 {
-    bt_side<<<spatial_grid(g, rows), dim3(TX, TY), 0, st>>>(G1, G2, E0, out, g, M, A, rows);
+    const bool dm = M.cd != 0.0, da = A.cd != 0.0;
+    const dim3 grid = spatial_grid(g, rows), block(TX, TY);
+    if (dm && da) bt_side<true, true><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
+    else if (dm) bt_side<true, false><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
+    else if (da) bt_side<false, true><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
+    else bt_side<false, false><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *T2, double *E0,
-                               Grid g, Stencil M, Stencil A, TCsr At, TCsr LT, TCsr Mt, TCsr L,
-                               int64_t r0, int64_t nr, int64_t nt, cudaStream_t st)
+                               Grid g, Stencil M, Stencil A, Tri4 tri, int64_t r0, int64_t nr,
+                               int64_t nt, cudaStream_t st)
 {
-    // temporal chunks: enough CTAs for ~8 per SM, at least 8 rows per chunk
+    // temporal chunks of 32 rows (2 halo rows of stencils recomputed per chunk)
     dim3 grid = spatial_grid(g, 1);
-    const int64_t tiles = (int64_t)grid.x * grid.y;
-    int64_t chunks = (148LL * 8 + tiles - 1) / tiles;
-    int chunk = (int)((nr + chunks - 1) / chunks);
-    if (chunk < 8) chunk = 8;
-    chunks = (nr + chunk - 1) / chunk;
+    const int chunk = 32;
+    const int64_t chunks = (nr + chunk - 1) / chunk;
     grid.z = (unsigned)(chunks < 65535 ? (chunks < 1 ? 1 : chunks) : 65535);
-    bside_fused<<<grid, dim3(TX, TY), 0, st>>>(U, u0, T1, T2, E0, g, M, A, At, LT, Mt, L, r0, nr,
-                                               nt, chunk);
+    const bool dm = M.cd != 0.0, da = A.cd != 0.0;
+    const dim3 block(TX, TY);
+    if (dm && da)
+        bside_fused<true, true><<<grid, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+    else if (dm)
+        bside_fused<true, false><<<grid, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+    else if (da)
+        bside_fused<false, true><<<grid, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+    else
+        bside_fused<false, false><<<grid, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
     return cudaGetLastError();
 }
 
