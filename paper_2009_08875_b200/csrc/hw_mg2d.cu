@@ -45,7 +45,12 @@ namespace hw {
 struct RingsDown { static constexpr int V0 = 4, V1 = 4, V2 = 4, V3 = 4, B = 8, R = 2, C = 0; };
 struct RingsUp { static constexpr int V0 = 4, V1 = 4, V2 = 4, V3 = 4, B = 8, R = 0, C = 4; };
 template <bool DOWN> using RingsOf = typename std::conditional<DOWN, RingsDown, RingsUp>::type;
-constexpr int kMaxWarpCarry = 4;       // warp totals summed for a chunk carry
+constexpr int kMaxWarpCarry = 4;       // warp totals summed for a chunk carry (exact path)
+constexpr int kChunkCarry = 8;         // chunk ends summed for a carry (truncated path)
+// narrow rows (<= 2 warps) always use the exact scan: measured faster, and the
+// chunk-end scratch would cost the n = 255 level one resident CTA per SM
+template <int NT> constexpr bool trunc_carry_ok() { return NT >= 128; }
+template <int NT> constexpr int chunk_end_words() { return trunc_carry_ok<NT>() ? 3 * (NT + kChunkCarry) : 0; }
 
 template <int P, int NT, bool DOWN>
 __host__ __device__ constexpr size_t stream_smem_words(int n)
@@ -54,7 +59,8 @@ __host__ __device__ constexpr size_t stream_smem_words(int n)
     const size_t W = (size_t)n + 2;
     const size_t Wc = (size_t)(n - 1) / 2 + 2;
     return W * (G::V0 + G::V1 + G::V2 + G::V3 + G::B + G::R + 1) + Wc * G::C +
-           3 * (size_t)(NT / 32 + kMaxWarpCarry) + (P + 1) + 33 + (kMaxWarpCarry + 1) + 8;
+           3 * (size_t)(NT / 32 + kMaxWarpCarry) + (size_t)chunk_end_words<NT>() + (P + 1) + 33 +
+           (kMaxWarpCarry + 1) + (kChunkCarry + 1) + 8;
 }
 
 // Row recurrence.  Thread t owns P consecutive points of a grid row; y_k is
@@ -73,6 +79,7 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
     using G = RingsOf<DOWN>;
     constexpr int NW = NT / 32;
     constexpr int KW = kMaxWarpCarry;
+    constexpr int KC = kChunkCarry;
     constexpr int MJ = (NT * P / 2 + NT - 1) / NT;      // coarse columns per thread (DOWN)
     extern __shared__ __align__(16) double sm[];
 
@@ -95,7 +102,8 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
     double *const zr = rs + G::R * W;                   // a row of zeros
     double *const cs = zr + W;                          // coarse ring (UP)
     double *const sc = cs + G::C * Wc;                  // warp totals [3][KW + NW]
-    double *const gp = sc + 3 * (NW + KW);              // beta^0..P, gamma^0..32, Gamma^0..KW
+    double *const se = sc + 3 * (NW + KW);              // chunk ends [3][KC + NT]
+    double *const gp = se + chunk_end_words<NT>();             // beta^0..P, gamma^0..32, Gamma^0..KW, w^0..KC
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j0 = tid * P;                             // first local column of this thread
@@ -110,6 +118,11 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
         Kw = ab >= 0.9 ? KW : (int)ceil(70.0 / (32.0 * P * -log2(ab)));
         Kw = Kw > KW ? KW : (Kw < 1 ? 1 : Kw);
     }
+    // truncated chunk carries: the nearest Kc chunk ends, gamma^Kc <= 2^-70
+    int Kc = 0;
+    if (ab > 0.0) Kc = ab >= 0.9 ? KC + 1 : (int)ceil(70.0 / (P * -log2(ab)));
+    constexpr bool kTruncOK = trunc_carry_ok<NT>();
+    const bool trunc = kTruncOK && Kc <= KC;            // uniform per CTA
     if (tid == 0) {
         double bp = 1.0;
         for (int k = 0; k <= P; ++k) { gp[k] = bp; bp *= beta; }
@@ -119,6 +132,8 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
         const double Gm = gp[P + 1 + 32];
         q = 1.0;
         for (int k = 0; k <= KW; ++k) { gp[P + 34 + k] = k < Kw ? q : 0.0; q *= Gm; }
+        q = 1.0;
+        for (int k = 0; k < KC; ++k) { gp[P + 35 + KW + k] = k < Kc ? q : 0.0; q *= g; }
     }
     {
         const int total = (int)(gp - sm);
@@ -135,6 +150,9 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
     double gscan[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) gscan[k] = gp[P + 1 + (1 << k)];
+    double wc[KC];                                      // gamma^(k) weights, 0 beyond Kc
+#pragma unroll
+    for (int k = 0; k < KC; ++k) wc[k] = gp[P + 35 + KW + k];
 
     constexpr int gs = DOWN ? 1 : -1;                   // UP runs point-reversed
     auto grow = [&](const double *base, int i) -> const double * {
@@ -285,32 +303,63 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
                 }
             }
 
-            // ---- exact warp scan of chunk ends T_l = S_l + gamma T_{l-1} ----
+            double carry[3];
+            auto exact_carry = [&]() {
+                // ---- exact warp scan of chunk ends T_l = S_l + gamma T_{l-1} ----
 #pragma unroll
-            for (int o = 1, q = 0; o < 32; o <<= 1, ++q) {
+                for (int o = 1, q = 0; o < 32; o <<= 1, ++q) {
+#pragma unroll
+                    for (int s = 0; s < 3; ++s) {
+                        const double v = __shfl_up_sync(0xffffffffu, S[s], o);
+                        if (lane >= o) S[s] = fma(gscan[q], v, S[s]);
+                    }
+                }
+                if (lane == 31) {
+#pragma unroll
+                    for (int s = 0; s < 3; ++s) sc[s * (NW + KW) + KW + warp] = S[s];
+                }
+                __syncthreads();                        // (#1) warp totals visible
 #pragma unroll
                 for (int s = 0; s < 3; ++s) {
-                    const double v = __shfl_up_sync(0xffffffffu, S[s], o);
-                    if (lane >= o) S[s] = fma(gscan[q], v, S[s]);
-                }
-            }
-            if (lane == 31) {
+                    const double *sp = sc + s * (NW + KW) + KW + warp;
+                    double Cw = 0.0;
 #pragma unroll
-                for (int s = 0; s < 3; ++s) sc[s * (NW + KW) + KW + warp] = S[s];
+                    for (int k = 0; k < KW; ++k) Cw = fma(Gw[k], sp[-1 - k], Cw);
+                    const double prev = __shfl_up_sync(0xffffffffu, S[s], 1);
+                    carry[s] = (lane == 0) ? Cw : fma(gl, Cw, prev);
+                }
+            };
+            if constexpr (kTruncOK) {
+                if (trunc) {
+                // ---- truncated carries: c_t = sum_{k=1..Kc} gamma^(k-1) S_{t-k} ----
+#pragma unroll
+                for (int s = 0; s < 3; ++s) se[s * (NT + KC) + KC + tid] = S[s];
+                __syncthreads();                        // (#1) chunk ends visible
+#pragma unroll
+                for (int s = 0; s < 3; ++s) {
+                    const double *sp = se + s * (NT + KC) + KC + tid;
+                    double part[KC / 2];
+#pragma unroll
+                    for (int k = 0; k < KC / 2; ++k)
+                        part[k] = fma(wc[2 * k + 1], sp[-2 * k - 2], wc[2 * k] * sp[-2 * k - 1]);
+#pragma unroll
+                    for (int w = KC / 4; w >= 1; w >>= 1)
+#pragma unroll
+                        for (int k = 0; k < w; ++k) part[k] += part[k + w];
+                    carry[s] = part[0];
+                }
+                } else {
+                    exact_carry();
+                }
+            } else {
+                exact_carry();
             }
-            __syncthreads();                            // (#1) warp totals visible
 
-            // ---- phase B: carries, write the swept rows ----
+            // ---- phase B: write the swept rows ----
             double *const Xrow = const_cast<double *>(grow(Xg, t - 4));
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
                 const int i = t - 2 * s;
-                const double *sp = sc + s * (NW + KW) + KW + warp;
-                double Cw = 0.0;
-#pragma unroll
-                for (int k = 0; k < KW; ++k) Cw = fma(Gw[k], sp[-1 - k], Cw);
-                const double prev = __shfl_up_sync(0xffffffffu, S[s], 1);
-                const double carry = (lane == 0) ? Cw : fma(gl, Cw, prev);
                 if (i < 0 || i > n) continue;           // row n is written as zeros
                 double *xr = (s == 0 ? SLOT(v1, G::V1, 0)
                                      : (s == 1 ? SLOT(v2, G::V2, 2) : SLOT(v3, G::V3, 4))) + 1 + j0;
@@ -322,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
 #pragma unroll
                 for (int k = 0; k < P; ++k) {
                     if (k < nvalid) {
-                        const double v = fma(bpow[k], carry, p[s][k]);
+                        const double v = fma(bpow[k], carry[s], p[s][k]);
                         xr[k] = v;
                         if (s == 2) Xrow[gs * (j0 + k)] = v;
                     }
