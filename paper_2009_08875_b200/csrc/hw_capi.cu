@@ -4,6 +4,7 @@
 // Each entry point replaces one call site of the reference package
 // (/root/reference/pkg/src/heatwave): see the header for the mapping.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -54,6 +55,7 @@ struct DevBand {           // a temporal factor in CSR on the device
 struct hwg_ctx {
     hwg_desc d{};
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
+    int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx
     int64_t rows_max = 0;              // MG batch capacity (rows)
     bool kernel_only = false;          // distributed-path context (no operator buffers)
@@ -314,6 +316,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.row_op = ro;
                 a.op = op;
                 a.zero_start = (l < c->K || cyc == 0) ? 1 : 0;
+                a.reg_ok = c->mg_reg_ok;
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
                 ProfScope ps(c, st, l == c->K ? 0 : 2,
                              8.0 * nr * (n2 * (a.zero_start ? 2 : 3) + m2));
@@ -342,6 +345,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.n = (1 << l) - 1;
                 a.row_op = ro;
                 a.op = op;
+                a.reg_ok = c->mg_reg_ok;
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
                 ProfScope ps(c, st, l == c->K ? 1 : 3, 8.0 * nr * (3 * n2 + m2));
                 CK(mg2d_stream_launch(a, false, nr, st));
@@ -438,6 +442,15 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     c->scale.assign(d.wavelet_scale, d.wavelet_scale + d.J);
     const int nops = d.J + 2;
     c->coef_host.assign(d.coef, d.coef + (size_t)nops * (d.K + 1) * HWG_COEF_STRIDE);
+    c->mg_reg_ok = 1;
+    for (int op = 0; op < nops; ++op)
+        for (int l = 1; l <= d.K; ++l) {
+            const double *cf = &c->coef_host[((size_t)op * (d.K + 1) + l) * HWG_COEF_STRIDE];
+            const double b = cf[kCy] * cf[kInv];
+            if (!(fabs(b) <= kRegBetaMax)) c->mg_reg_ok = 0;
+        }
+    if (const char *ev = getenv("HWG_MG_REG"))      // A/B switch for measurements
+        if (ev[0] == '0') c->mg_reg_ok = 0;
     int rc;
 #define GO(x)                      \
     do {                           \

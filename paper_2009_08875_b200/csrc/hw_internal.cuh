@@ -20,6 +20,7 @@ struct MgStreamArgs {
     const int32_t *row_op;              // per temporal row, or null
     int op;                             // default operator
     int zero_start;                     // DOWN: iterate starts at zero
+    int reg_ok;                         // |beta| small enough for mg2d_reg
 };
 
 struct MgCoarseArgs {
@@ -37,6 +38,10 @@ struct MgCoarseArgs {
 
 constexpr int kCoarseTop2d = 5;
 cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
+// register-resident variant (hw_mg2d_reg.cu), levels 7..10; cudaErrorNotSupported otherwise
+cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
+// largest |beta| = |cy / c0| mg2d_reg accepts (8-chunk window: |beta|^32 <= 2^-60)
+constexpr double kRegBetaMax = 0.2726;
 cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st);
 
 // ---- hw_mg1d.cu ----------------------------------------------------------

@@ -584,6 +584,10 @@ cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, c
     // warp's 64-bit shared loads at stride 8P bytes are bank-conflict free
     // (P = 5 measured faster than P = 3 with 11 warps at n = 1023)
     const int n = a.n;
+    if (a.reg_ok) {
+        const cudaError_t e = mg2d_reg_launch(a, down, rows, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (n <= 96)
         return down ? launch_stream_t<3, 32, true>(a, rows, st) : launch_stream_t<3, 32, false>(a, rows, st);
     if (n <= 160)
