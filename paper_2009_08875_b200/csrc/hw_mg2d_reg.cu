@@ -1,5 +1,5 @@
 // hw_mg2d_reg.cu -- register-resident streamed multigrid level passes, 2D,
-// levels l = 7..10 (n = 2^l - 1 = 4 NT - 1 points per direction).
+// levels l = 7..10 (n = 2^l - 1 = P NT - 1 points per direction).
 //
 // Same operator as mg2d_stream (hw_mg2d.cu; the reference's _mg_core,
 // /root/reference/pkg/src/heatwave/_kernels.py:110-199): per temporal row,
@@ -9,24 +9,25 @@
 // temporal row's grid, one grid row per step, the three sweeps pipelined two
 // grid rows apart.  What differs from mg2d_stream is where the state lives:
 //
-//  * Thread t owns columns 4t..4t+3 of every grid row (n + 1 = 4 NT, so no
-//    thread idles).  The swept rows each sweep still needs (two per sweep)
-//    live in REGISTERS; only chunk-boundary values cross threads -- by
-//    shuffles inside a warp and through a few shared-memory words between
-//    neighbouring warps (written before a barrier, read after it).
+//  * Thread t owns columns P t .. P t + P-1 of every grid row (n + 1 = P NT,
+//    no thread idles).  The swept rows each sweep still needs (two per sweep)
+//    live in REGISTERS; only chunk-boundary values cross threads.
 //  * A sweep over grid row i is the recurrence x_j = p_j + beta x_{j-1}
 //    (p_j: right-hand side minus the known neighbours, scaled by 1/c0).  Each
-//    thread runs it over its 4 points from a zero carry (chunk end S); the
+//    thread runs it over its P points from a zero carry (chunk end S); the
 //    carry into chunk t is T_{t-1} = sum_k gamma^(k-1) S_{t-k}, gamma =
-//    beta^4.  A 3-level shuffle scan sums the nearest 8 chunk ends inside the
+//    beta^P.  A shuffle scan sums the nearest W = 32/P chunk ends inside the
 //    warp; the previous warp's windowed total covers the rest.  |beta| <=
 //    1/4 for alpha A + mu M in 2D (checked on the host, else mg2d_stream is
-//    used), so the dropped tail is below gamma^8 = 2^-64 relative: the
+//    used), so the dropped tail is below gamma^W <= 2^-64 relative: the
 //    lexicographic GS result up to rounding.
+//  * The carry into chunk t IS the new value of the point left of the chunk,
+//    so left halos cost nothing; right halos (the next chunk's first new
+//    value) are one shuffle, or a shared word at a warp edge.
 //  * DOWN's residual after the third sweep uses the GS identity
 //      r(i,j) = -(cy d(i,j+1) + cx d(i+1,j) + cd d(i+1,j+1)),  d = x3 - x2,
-//    (every point's equation held exactly when it was updated; only its
-//    "upper" neighbours moved afterwards) -- 3 multiply-adds per point.
+//    (every point's equation held when it was updated; only its "upper"
+//    neighbours moved afterwards) -- 3 multiply-adds per point.
 //  * b, the input iterate and (UP) the coarse correction are staged by
 //    zero-filling cp.async into THREAD-PRIVATE shared-memory slots three
 //    steps ahead, so they need no barrier; each step has two barriers
@@ -37,8 +38,6 @@
 namespace hw {
 namespace {
 
-constexpr int RP = 4;  // points per thread
-
 HW_DEV void cp_async8z(void *smem, const void *gmem, bool valid)
 {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -46,48 +45,71 @@ HW_DEV void cp_async8z(void *smem, const void *gmem, bool valid)
                  "r"(valid ? 8 : 0));
 }
 
-// shared-memory words (doubles) of one CTA
-template <int NT, bool DOWN, bool ZS>
+constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
+// shared-memory words (doubles) of one CTA.  Fine rows are staged whole
+// (cooperative, coalesced copies) in slots of RS words with a 16-byte-unit
+// XOR swizzle, so a thread's own chunk reads are conflict-free LDS.128.
+template <int P, int NT, bool DOWN, bool ZS>
 struct RegSmem {
     static constexpr int NW = NT / 32;
-    static constexpr int B = 8 * 2 * NT * 2;                 // b ring  [8][2][NT][2]
-    static constexpr int X0 = (DOWN && ZS) ? 0 : 4 * 5 * NT;  // x0 ring [4][5][NT]
-    static constexpr int C = DOWN ? 0 : 4 * 4 * NT;          // coarse  [4][4][NT]
-    static constexpr int H = 11 * (NW + 1);                  // halos, carries
-    static constexpr int total = B + X0 + C + H;
+    static constexpr int RS = P * NT + 16;                  // fine row slot
+    static constexpr int CS = P * NT / 2 + 8;               // coarse row slot
+    // ring depths: copies are issued after the step's second barrier, when
+    // the slot's previous row (b: t-4, x0: t+1) has been consumed
+    static constexpr int NB = 7, NX = 3, NCR = 3;
+    static constexpr int B = NB * RS;                       // b ring
+    static constexpr int X0 = (DOWN && ZS) ? 0 : NX * RS;   // x0 ring
+    static constexpr int C = DOWN ? 0 : NCR * CS;           // coarse ring (UP)
+    static constexpr int O = RS;                            // output row
+    static constexpr int H = 7 * (NW + 1);                  // halos, carries
+    static constexpr int total = B + X0 + C + O + H;
 };
 
-template <int NT, bool DOWN, bool ZS>
+template <int P, int NT, bool DOWN, bool ZS>
 struct RegPass {
-    static constexpr int P = RP;
     static constexpr int NW = NT / 32;
     static constexpr int n = P * NT - 1;
     static constexpr int m = (n - 1) / 2;
-    using SM = RegSmem<NT, DOWN, ZS>;
+    static constexpr int WIN = 32 / P;                 // chunk ends in the carry window
+    static constexpr int LEV = ilog2c(WIN);            // shuffle-scan levels
+    static constexpr int NC = P / 2 + 2;               // coarse columns a thread reads
+    static constexpr int HS = NW + 1;
+    static constexpr int SWZ = P / 2 - 1;
+    using SM = RegSmem<P, NT, DOWN, ZS>;
+    static constexpr int RS = SM::RS, CS = SM::CS;
+    static_assert(P % 2 == 0 && 32 % P == 0 && P >= 4 && NC % 2 == 0 && CS >= m + 2, "chunk layout");
+    static constexpr int gs = DOWN ? 1 : -1;           // UP runs point-reversed
 
-    // ---- per-CTA constants ----
-    const MgStreamArgs &a;
+    // ---- per-CTA / per-thread constants ----
     int tid, lane, warp;
     bool last;                            // owns column n (a zero pad)
     double cx, cy, cd, inv, beta;
-    double bp[4];                         // beta^(k+1)
-    double w1, w2, w4, gl;                // scan weights, gamma^lane
-    const double *Bg;
-    double *Xg;
-    const double *Xcg;
-    double *Bcg;
-    double *bsm, *x0sm, *csm;
-    double *HL, *HR, *HRes, *tot;         // [3][NW+1], [3][NW+1], [2][NW+1], [3][NW+1]
+    double bp[P];                         // beta^(k+1)
+    double wl[LEV];                       // scan weights gamma^(2^l) (0 below lane 2^l)
+    double gl;                            // gamma^lane
+    const double *Bg, *Xcg;               // row 0 of this temporal row's level arrays
+    double *Xg, *Bcg;
+    double *bsm, *x0sm, *csm, *osm;
+    double *HR, *HRes, *tot;              // [3][HS], [1][HS], [3][HS]
 
     // ---- register state ----
-    double X1[2][4], X1L, X1R[2];          // sweep-1 rows (slot = row & 1) + halos
-    double X2[2][4], X2L, X2R[2];
-    double X3[4], X3L;                     // last sweep-3 row
-    double D[2][4], DR[2];                 // DOWN: x3 - x2 rows
-    double X0n[5];                         // x0 row t (+ right halo)
-    double acc[2];                         // DOWN: coarse accumulators
+    double X1[2][P], X1L, X1R[2];          // sweep-1 rows (slot = row & 1) + halos
+    double X2[2][P], X2L, X2R[2];
+    double X3[P], X3L;                     // last sweep-3 row
+    double D[2][P], DR[2];                 // DOWN: x3 - x2 rows
+    double X0n[P + 1];                     // x0 row t (+ right halo)
+    double acc[P / 2];                     // DOWN: coarse accumulators
 
-    HW_DEV RegPass(const MgStreamArgs &a_, double *sm) : a(a_)
+    // swizzled slot position of fine column j (16-byte units permuted within
+    // groups of 8 so 8 consecutive threads' chunk units hit distinct banks)
+    static HW_DEV int phys(int j)
+    {
+        const int u = j >> 1;
+        return ((u ^ ((u >> 3) & SWZ)) << 1) | (j & 1);
+    }
+
+    HW_DEV RegPass(const MgStreamArgs &a, double *sm)
     {
         tid = threadIdx.x;
         lane = tid & 31;
@@ -103,152 +125,172 @@ struct RegPass {
         beta = -cy * inv;
         double q = 1.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) { q *= beta; bp[k] = q; }
-        const double g = bp[3], g2 = g * g, g4 = g2 * g2;
-        w1 = lane >= 1 ? g : 0.0;
-        w2 = lane >= 2 ? g2 : 0.0;
-        w4 = lane >= 4 ? g4 : 0.0;
-        double gp = 1.0, gb = g;               // gamma^lane by binary powering
+        for (int k = 0; k < P; ++k) { q *= beta; bp[k] = q; }
+        double g = bp[P - 1];
+#pragma unroll
+        for (int l = 0; l < LEV; ++l) { wl[l] = lane >= (1 << l) ? g : 0.0; g *= g; }
+        double gp = 1.0, gb = bp[P - 1];       // gamma^lane by binary powering
 #pragma unroll
         for (int b = 0; b < 5; ++b) { if (lane & (1 << b)) gp *= gb; gb *= gb; }
         gl = gp;
         Bg = a.B + row * a.ldB;
         Xg = a.X + row * a.ldX;
         Xcg = DOWN ? nullptr : a.Xc + row * a.ldXc;
-        Bcg = DOWN ? a.Bc + row * a.ldBc : nullptr;
+        Bcg = DOWN ? a.Bc + row * a.ldBc + (P / 2) * tid : nullptr;
         bsm = sm;
         x0sm = bsm + SM::B;
         csm = x0sm + SM::X0;
-        HL = csm + SM::C;
-        HR = HL + 3 * (NW + 1);
-        HRes = HR + 3 * (NW + 1);
-        tot = HRes + 2 * (NW + 1);
-        for (int k = tid; k < SM::H; k += NT) HL[k] = 0.0;
+        osm = csm + SM::C;
+        HR = osm + SM::O;
+        HRes = HR + 3 * HS;
+        tot = HRes + HS;
+        for (int k = tid; k < SM::H; k += NT) HR[k] = 0.0;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) X1[s][k] = X2[s][k] = D[s][k] = 0.0;
+            for (int k = 0; k < P; ++k) X1[s][k] = X2[s][k] = D[s][k] = 0.0;
             X1R[s] = X2R[s] = DR[s] = 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) X3[k] = 0.0;
+        for (int k = 0; k < P; ++k) X3[k] = 0.0;
         X1L = X2L = X3L = 0.0;
 #pragma unroll
-        for (int e = 0; e < 5; ++e) X0n[e] = 0.0;
-        acc[0] = acc[1] = 0.0;
+        for (int e = 0; e <= P; ++e) X0n[e] = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < P / 2; ++q2) acc[q2] = 0.0;
     }
 
-    // global element (grid row i, local column j) of a level array; UP runs
-    // point-reversed
-    HW_DEV int64_t gidx(int i, int j) const
+    // ring slot of row i (i >= -3)
+    static HW_DEV int ring(int i, int R) { return (i + 3 * R) % R; }
+
+    // global element of (grid row i, local column j); UP is point-reversed
+    static HW_DEV int64_t gidx(int i, int j)
     {
         return DOWN ? (int64_t)i * n + j : (int64_t)(n - 1 - i) * n + (n - 1 - j);
     }
 
-    // zero-filling stages of b row ib, x0 row ix, (UP) coarse row ic
-    HW_DEV void issue_b(int ib) const
+    // cooperative zero-filling stage of fine row i (columns 0..n+1) of src
+    HW_DEV void stage_row(double *slot, const double *src, int i) const
     {
-        const int j0 = P * tid;
-        const bool vr = ib < n;
-        double *dst = bsm + (size_t)(ib & 7) * 4 * NT;
+        const bool vr = i < n;
+        const double *base = src + (vr ? gidx(i, 0) : 0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool v = vr && (j0 + k < n);
-            cp_async8z(dst + ((k >> 1) * NT + tid) * 2 + (k & 1), Bg + (v ? gidx(ib, j0 + k) : 0), v);
+        for (int k = 0; k < (P * NT + 2 + NT - 1) / NT; ++k) {
+            const int j = tid + k * NT;
+            if (j < P * NT + 2) {
+                const bool v = vr && j < n;
+                cp_async8z(slot + phys(j), base + (v ? gs * j : 0), v);
+            }
         }
     }
-    HW_DEV void issue_x0(int ix) const
+    // coarse row ic, local columns -1..m at slot index J+1 (zeros outside)
+    HW_DEV void stage_coarse(int ic) const
     {
-        const int j0 = P * tid;
-        const bool vr = ix < n;
-        double *dst = x0sm + (size_t)(ix & 3) * 5 * NT + tid;
-#pragma unroll
-        for (int e = 0; e < 5; ++e) {
-            const bool v = vr && (j0 + e < n);
-            cp_async8z(dst + e * NT, Xg + (v ? gidx(ix, j0 + e) : 0), v);
-        }
-    }
-    HW_DEV void issue_c(int ic) const
-    {
-        // coarse columns 2t-1 .. 2t+2, point-reversed like the fine grid
         const bool vr = ic >= 0 && ic < m;
-        double *dst = csm + (size_t)(ic & 3) * 4 * NT + tid;
+        double *slot = csm + (size_t)ring(ic, SM::NCR) * CS;
+        const double *base = Xcg + (vr ? (int64_t)(m - 1 - ic) * m + (m - 1) : 0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int J = 2 * tid - 1 + q;
-            const bool v = vr && J >= 0 && J < m;
-            cp_async8z(dst + q * NT, Xcg + (v ? (int64_t)(m - 1 - ic) * m + (m - 1 - J) : 0), v);
+        for (int k = 0; k < (m + 2 + NT - 1) / NT; ++k) {
+            const int J = tid + k * NT - 1;
+            if (J <= m) {
+                const bool v = vr && J >= 0 && J < m;
+                cp_async8z(slot + J + 1, base - (v ? J : 0), v);
+            }
         }
     }
     // the group step t issues: b(t+3), x0(t+4) and the coarse row x0(t+4) adds
     HW_DEV void issue(int t) const
     {
-        issue_b(t + 3);
-        if constexpr (!(DOWN && ZS)) issue_x0(t + 4);
+        stage_row(bsm + (size_t)ring(t + 3, SM::NB) * RS, Bg, t + 3);
+        if constexpr (!(DOWN && ZS)) stage_row(x0sm + (size_t)ring(t + 4, SM::NX) * RS, Xg, t + 4);
         if constexpr (!DOWN) {
-            if (!((t + 4) & 1)) issue_c((t + 4) / 2);
+            if (!((t + 4) & 1)) stage_coarse((t + 4) / 2);
         }
         cp_async_commit();
     }
 
-    // x0 row i (5 values) from its slot; UP adds the prolongated coarse
-    // correction (same arithmetic as mg2d_stream's prolongate)
-    template <int IPAR, bool EDGE>
-    HW_DEV void load_x0(int i, double v[5]) const
+    // own chunk (P values) of a staged row
+    HW_DEV void load_chunk(const double *slot, double v[P]) const
     {
-        const double *src = x0sm + (size_t)(i & 3) * 5 * NT + tid;
 #pragma unroll
-        for (int e = 0; e < 5; ++e) v[e] = src[e * NT];
-        if constexpr (!DOWN) {
-            if (EDGE && i >= n) return;                  // row n stays a zero pad
-            double ca[4], cb[4];
-            const int c_a = IPAR ? (i - 1) / 2 : i / 2 - 1;
-            const double *pa = csm + (size_t)(c_a & 3) * 4 * NT + tid;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) ca[q] = pa[q * NT];
-            double pv[5];
-            if constexpr (IPAR) {
-                pv[0] = 0.5 * ca[0] + 0.5 * ca[1];
-                pv[1] = ca[1];
-                pv[2] = 0.5 * ca[1] + 0.5 * ca[2];
-                pv[3] = ca[2];
-                pv[4] = 0.5 * ca[2] + 0.5 * ca[3];
-            } else {
-                const double *pb = csm + (size_t)((c_a + 1) & 3) * 4 * NT + tid;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) cb[q] = pb[q * NT];
-                pv[0] = 0.5 * ca[0] + 0.5 * cb[1];
-                pv[1] = 0.5 * ca[1] + 0.5 * cb[1];
-                pv[2] = 0.5 * ca[1] + 0.5 * cb[2];
-                pv[3] = 0.5 * ca[2] + 0.5 * cb[2];
-                pv[4] = 0.5 * ca[2] + 0.5 * cb[3];
-            }
-#pragma unroll
-            for (int e = 0; e < 5; ++e) v[e] = v[e] + pv[e];
-            if (last) v[3] = v[4] = 0.0;                 // columns n, n+1
+        for (int h = 0; h < P / 2; ++h) {
+            const int u = (P / 2) * tid + h;
+            const double2 w = *reinterpret_cast<const double2 *>(slot + ((u ^ ((u >> 3) & SWZ)) << 1));
+            v[2 * h] = w.x;
+            v[2 * h + 1] = w.y;
         }
     }
 
-    HW_DEV void load_b(int i, double b[4]) const
+    // x0 row i (P+1 values) from its slot; UP adds the prolongated coarse
+    // correction (same arithmetic as mg2d_stream's prolongate)
+    template <int IPAR, bool EDGE>
+    HW_DEV void load_x0(int i, double v[P + 1]) const
     {
-        const double2 *src = reinterpret_cast<const double2 *>(bsm + (size_t)(i & 7) * 4 * NT);
-        const double2 lo = src[tid], hi = src[NT + tid];
-        b[0] = lo.x;
-        b[1] = lo.y;
-        b[2] = hi.x;
-        b[3] = hi.y;
+        const double *slot = x0sm + (size_t)ring(i, SM::NX) * RS;
+        load_chunk(slot, v);
+        v[P] = slot[phys(P * (tid + 1))];
+        if constexpr (!DOWN) {
+            if (EDGE && i >= n) return;                  // row n stays a zero pad
+            double ca[NC], cb[NC];
+            const int c_a = IPAR ? (i - 1) / 2 : i / 2 - 1;
+            const double *pa = csm + (size_t)ring(c_a, SM::NCR) * CS + (P / 2) * tid;
+#pragma unroll
+            for (int q = 0; q < NC; q += 2) {
+                const double2 w = *reinterpret_cast<const double2 *>(pa + q);
+                ca[q] = w.x;
+                ca[q + 1] = w.y;
+            }
+            if constexpr (!IPAR) {
+                const double *pb = csm + (size_t)ring(c_a + 1, SM::NCR) * CS + (P / 2) * tid;
+#pragma unroll
+                for (int q = 0; q < NC; q += 2) {
+                    const double2 w = *reinterpret_cast<const double2 *>(pb + q);
+                    cb[q] = w.x;
+                    cb[q + 1] = w.y;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e <= P; ++e) {
+                double pv;
+                if (e & 1) {
+                    const int q = (e + 1) / 2;
+                    pv = IPAR ? ca[q] : 0.5 * ca[q] + 0.5 * cb[q];
+                } else {
+                    const int q = e / 2;
+                    pv = IPAR ? 0.5 * ca[q] + 0.5 * ca[q + 1] : 0.5 * ca[q] + 0.5 * cb[q + 1];
+                }
+                v[e] = v[e] + pv;
+            }
+            if (last) v[P - 1] = v[P] = 0.0;             // columns n, n+1
+        }
     }
 
-    // zero-carry chunk recurrence of one sweep over the thread's 4 points
-    HW_DEV void chunk(const double u[4], double uL, const double c[4], double cR,
-                      const double d[4], double dR, const double b[4], double y[4]) const
+    HW_DEV void load_b(int i, double b[P]) const
+    {
+        load_chunk(bsm + (size_t)ring(i, SM::NB) * RS, b);
+    }
+
+    // coalesced copy of the staged output row (grid row i) to global memory
+    HW_DEV void flush(int i) const
+    {
+        double *dst = Xg + gidx(i, 0);
+#pragma unroll
+        for (int k = 0; k < (n + NT - 1) / NT; ++k) {
+            const int j = tid + k * NT;
+            if (j < n) dst[gs * j] = osm[phys(j)];
+        }
+    }
+
+    // zero-carry chunk recurrence of one sweep over the thread's P points
+    HW_DEV void chunk(const double u[P], double uL, const double c[P], double cR,
+                      const double d[P], double dR, const double b[P], double y[P]) const
     {
         double yy = 0.0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < P; ++k) {
             const double ul = k ? u[k - 1] : uL;
-            const double cr = k < 3 ? c[k + 1] : cR;
-            const double dr = k < 3 ? d[k + 1] : dR;
+            const double cr = k < P - 1 ? c[k + 1] : cR;
+            const double dr = k < P - 1 ? d[k + 1] : dR;
             const double e1 = fma(-cd, ul, b[k]);
             const double e2 = u[k] + d[k];
             const double e3 = fma(cd, dr, cy * cr);
@@ -259,9 +301,8 @@ struct RegPass {
 
     HW_DEV double wscan(double s) const
     {
-        s = fma(w1, __shfl_up_sync(0xffffffffu, s, 1), s);
-        s = fma(w2, __shfl_up_sync(0xffffffffu, s, 2), s);
-        s = fma(w4, __shfl_up_sync(0xffffffffu, s, 4), s);
+#pragma unroll
+        for (int l = 0; l < LEV; ++l) s = fma(wl[l], __shfl_up_sync(0xffffffffu, s, 1 << l), s);
         return s;
     }
 
@@ -273,34 +314,30 @@ struct RegPass {
         const bool v2 = !EDGE || (t >= 2 && t - 2 < n);
         const bool v3 = !EDGE || (t >= 4 && t - 4 < n);
         const bool vr = DOWN && (!EDGE || (t >= 6 && t - 6 < n));
+        const bool vo = !EDGE || (t >= 5 && t - 5 < n);
 
-        cp_async_wait<2>();                              // own b(t), x0(t+1) landed
-        __syncthreads();                                 // (A) halos of step t-1 visible
-        issue(t);
-        if (lane == 0) {
-            X1L = HL[0 * (NW + 1) + warp];
-            X2L = HL[1 * (NW + 1) + warp];
-            X3L = HL[2 * (NW + 1) + warp];
-        }
+        cp_async_wait<2>();                              // own copies of step t-3 landed
+        __syncthreads();                                 // (A) all copies, halos, output row visible
+        if (vo) flush(t - 5);                            // row t-5, staged last step
         if (lane == 31) {
-            X1R[Q] = HR[0 * (NW + 1) + warp + 1];
-            X2R[Q] = HR[1 * (NW + 1) + warp + 1];
-            if constexpr (DOWN) DR[Q] = HR[2 * (NW + 1) + warp + 1];
+            X1R[Q] = HR[0 * HS + warp + 1];
+            X2R[Q] = HR[1 * HS + warp + 1];
+            if constexpr (DOWN) DR[Q] = HR[2 * HS + warp + 1];
         }
 
         // ---- phase A: chunk recurrences of the three sweeps ----
-        double y[3][4], b[4];
-        double dn0[5];
+        double y[3][P], b[P];
+        double dn0[P + 1];
         if constexpr (DOWN && ZS) {
-            const double z[4] = {0.0, 0.0, 0.0, 0.0};
+            double z[P];
+#pragma unroll
+            for (int k = 0; k < P; ++k) z[k] = 0.0;
             load_b(t, b);
             chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0]);
-#pragma unroll
-            for (int e = 0; e < 5; ++e) dn0[e] = 0.0;
         } else {
             load_x0<Q, EDGE>(t + 1, dn0);
             load_b(t, b);
-            chunk(X1[Q], X1L, X0n, X0n[4], dn0, dn0[4], b, y[0]);
+            chunk(X1[Q], X1L, X0n, X0n[P], dn0, dn0[P], b, y[0]);
         }
         load_b(t - 2, b);
         chunk(X2[Q], X2L, X1[PAR], X1R[PAR], X1[Q], X1R[Q], b, y[1]);
@@ -308,102 +345,96 @@ struct RegPass {
         chunk(X3, X3L, X2[PAR], X2R[PAR], X2[Q], X2R[Q], b, y[2]);
 
         // residual of grid row t-6 from d(t-6), d(t-5)
-        double R[4];
+        double R[P];
         if constexpr (DOWN) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double d6r = k < 3 ? D[PAR][k + 1] : DR[PAR];
-                const double d5r = k < 3 ? D[Q][k + 1] : DR[Q];
+            for (int k = 0; k < P; ++k) {
+                const double d6r = k < P - 1 ? D[PAR][k + 1] : DR[PAR];
+                const double d5r = k < P - 1 ? D[Q][k + 1] : DR[Q];
                 R[k] = fma(-cy, d6r, fma(-cx, D[Q][k], -cd * d5r));
             }
-            if (lane == 31) {
-                HRes[warp + 1] = R[2];
-                HRes[(NW + 1) + warp + 1] = R[3];
-            }
+            if (lane == 0) HRes[warp] = R[0];
         }
 
         double A[3];
 #pragma unroll
-        for (int s = 0; s < 3; ++s) A[s] = wscan(y[s][3]);
+        for (int s = 0; s < 3; ++s) A[s] = wscan(y[s][P - 1]);
         if (lane == 31) {
 #pragma unroll
-            for (int s = 0; s < 3; ++s) tot[s * (NW + 1) + warp + 1] = A[s];
+            for (int s = 0; s < 3; ++s) tot[s * HS + warp + 1] = A[s];
         }
-        __syncthreads();                                 // (B) warp totals visible
+        __syncthreads();                                 // (B) warp totals visible, output row
+                                                         //     and the oldest ring slots free
+        issue(t);
 
         // ---- phase B: carries, new rows, halos ----
-        double xn[3][4];
+        double xn[3][P], cin[3];
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
             const double prev = __shfl_up_sync(0xffffffffu, A[s], 1);
-            const double cin = fma(gl, tot[s * (NW + 1) + warp], lane ? prev : 0.0);
+            cin[s] = fma(gl, tot[s * HS + warp], lane ? prev : 0.0);
             const bool vs = s == 0 ? v1 : (s == 1 ? v2 : v3);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double v = fma(bp[k], cin, y[s][k]);
-                xn[s][k] = (vs && !(k == 3 && last)) ? v : 0.0;
+            for (int k = 0; k < P; ++k) {
+                const double v = fma(bp[k], cin[s], y[s][k]);
+                xn[s][k] = (vs && !(k == P - 1 && last)) ? v : 0.0;
             }
+            if (!vs) cin[s] = 0.0;
         }
-        double dl[4];
+        double dl[P];
         if constexpr (DOWN) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) dl[k] = xn[2][k] - X2[PAR][k];
+            for (int k = 0; k < P; ++k) dl[k] = xn[2][k] - X2[PAR][k];
         }
-        if (v3) {                                        // final values of row t-4
-            const int j0 = P * tid;
+        // stage the final values of row t-4 for next step's coalesced flush
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (k < 3 || !last) Xg[gidx(t - 4, j0 + k)] = xn[2][k];
+        for (int h = 0; h < P / 2; ++h) {
+            const int u = (P / 2) * tid + h;
+            *reinterpret_cast<double2 *>(osm + ((u ^ ((u >> 3) & SWZ)) << 1)) =
+                make_double2(xn[2][2 * h], xn[2][2 * h + 1]);
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < P; ++k) {
             X1[PAR][k] = xn[0][k];
             X2[PAR][k] = xn[1][k];
             X3[k] = xn[2][k];
             if constexpr (DOWN) D[PAR][k] = dl[k];
         }
-        X1L = __shfl_up_sync(0xffffffffu, xn[0][3], 1);
-        X2L = __shfl_up_sync(0xffffffffu, xn[1][3], 1);
-        X3L = __shfl_up_sync(0xffffffffu, xn[2][3], 1);
+        // left halo = the carry (the new value left of the chunk)
+        X1L = cin[0];
+        X2L = cin[1];
+        X3L = cin[2];
         X1R[PAR] = __shfl_down_sync(0xffffffffu, xn[0][0], 1);
         X2R[PAR] = __shfl_down_sync(0xffffffffu, xn[1][0], 1);
         if constexpr (DOWN) DR[PAR] = __shfl_down_sync(0xffffffffu, dl[0], 1);
-        if (lane == 31) {
-            HL[0 * (NW + 1) + warp + 1] = xn[0][3];
-            HL[1 * (NW + 1) + warp + 1] = xn[1][3];
-            HL[2 * (NW + 1) + warp + 1] = xn[2][3];
-        }
         if (lane == 0) {
-            HR[0 * (NW + 1) + warp] = xn[0][0];
-            HR[1 * (NW + 1) + warp] = xn[1][0];
-            if constexpr (DOWN) HR[2 * (NW + 1) + warp] = dl[0];
+            HR[0 * HS + warp] = xn[0][0];
+            HR[1 * HS + warp] = xn[1][0];
+            if constexpr (DOWN) HR[2 * HS + warp] = dl[0];
         }
         if constexpr (!(DOWN && ZS)) {
 #pragma unroll
-            for (int e = 0; e < 5; ++e) X0n[e] = dn0[e];
+            for (int e = 0; e <= P; ++e) X0n[e] = dn0[e];
         }
 
         // ---- restriction of residual row r = t-6 (parity PAR) ----
+        // coarse column J = (P/2) t + q collects fine columns 2J, 2J+1, 2J+2
         if constexpr (DOWN) {
             if (vr) {
-                double RL2 = __shfl_up_sync(0xffffffffu, R[2], 1);
-                double RL3 = __shfl_up_sync(0xffffffffu, R[3], 1);
-                if (lane == 0) {
-                    RL2 = HRes[warp];
-                    RL3 = HRes[(NW + 1) + warp];
-                }
+                double RR = __shfl_down_sync(0xffffffffu, R[0], 1);
+                if (lane == 31) RR = HRes[warp + 1];
                 const int r = t - 6;
-                if constexpr (PAR) {                     // centre row of coarse (r-1)/2
-                    acc[0] += fma(0.5, RL2 + R[0], RL3);
-                    acc[1] += fma(0.5, R[0] + R[2], R[1]);
-                } else {                                 // bottom of r/2-1, top of r/2
-                    if (r >= 2) {
-                        double *bc = Bcg + (int64_t)(r / 2 - 1) * m + 2 * tid;
-                        if (tid > 0) bc[-1] = acc[0] + 0.5 * (RL3 + R[0]);
-                        bc[0] = acc[1] + 0.5 * (R[1] + R[2]);
+#pragma unroll
+                for (int q = 0; q < P / 2; ++q) {
+                    const double r0 = R[2 * q], r1 = R[2 * q + 1];
+                    const double r2 = 2 * q + 2 < P ? R[2 * q + 2] : RR;
+                    if constexpr (PAR) {                 // centre row of coarse (r-1)/2
+                        acc[q] += fma(0.5, r0 + r2, r1);
+                    } else {                             // bottom of r/2-1, top of r/2
+                        if (r >= 2 && (q < P / 2 - 1 || !last))
+                            Bcg[(int64_t)(r / 2 - 1) * m + q] = acc[q] + 0.5 * (r1 + r2);
+                        acc[q] = 0.5 * (r0 + r1);
                     }
-                    acc[0] = 0.5 * (RL2 + RL3);
-                    acc[1] = 0.5 * (R[0] + R[1]);
                 }
             }
         }
@@ -414,21 +445,23 @@ struct RegPass {
         // prologue: x0 row 0 (+ coarse rows -1, 0), then the groups steps
         // -3..-1 would have issued
         if constexpr (!(DOWN && ZS)) {
-            issue_x0(0);
+            stage_row(x0sm, Xg, 0);
             if constexpr (!DOWN) {
-                issue_c(-1);
-                issue_c(0);
+                stage_coarse(-1);
+                stage_coarse(0);
             }
             cp_async_commit();
         }
         issue(-3);
         issue(-2);
-        issue(-1);
         if constexpr (!(DOWN && ZS)) {
-            cp_async_wait<3>();
+            cp_async_wait<2>();
+            __syncthreads();
             load_x0<0, true>(0, X0n);
+            __syncthreads();                             // x0(3) reuses x0(0)'s slot
         }
-        constexpr int nsteps = DOWN ? n + 6 : n + 4;
+        issue(-1);
+        constexpr int nsteps = DOWN ? n + 6 : n + 5;     // the last flush is step n+4
         int t = 0;
         for (; t < 6; t += 2) {
             step<true, 0>(t);
@@ -446,31 +479,31 @@ struct RegPass {
     }
 };
 
-template <int NT, bool DOWN, bool ZS>
-__global__ void __launch_bounds__(NT, 1) mg2d_reg(MgStreamArgs a)
+template <int P, int NT, bool DOWN, bool ZS, int MINB>
+__global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
 {
     extern __shared__ __align__(16) double sm[];
-    RegPass<NT, DOWN, ZS> p(a, sm);
+    RegPass<P, NT, DOWN, ZS> p(a, sm);
     p.run();
 }
 
-template <int NT, bool DOWN, bool ZS>
+template <int P, int NT, bool DOWN, bool ZS, int MINB>
 cudaError_t launch_reg_t(const MgStreamArgs &a, int64_t rows, cudaStream_t st)
 {
-    const size_t smem = RegSmem<NT, DOWN, ZS>::total * sizeof(double);
-    auto k = mg2d_reg<NT, DOWN, ZS>;
+    const size_t smem = RegSmem<P, NT, DOWN, ZS>::total * sizeof(double);
+    auto k = mg2d_reg<P, NT, DOWN, ZS, MINB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)rows, NT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int NT>
+template <int P, int NT, int MINB>
 cudaError_t launch_reg_n(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
-    if (!down) return launch_reg_t<NT, false, false>(a, rows, st);
-    return a.zero_start ? launch_reg_t<NT, true, true>(a, rows, st)
-                        : launch_reg_t<NT, true, false>(a, rows, st);
+    if (!down) return launch_reg_t<P, NT, false, false, MINB>(a, rows, st);
+    return a.zero_start ? launch_reg_t<P, NT, true, true, MINB>(a, rows, st)
+                        : launch_reg_t<P, NT, true, false, MINB>(a, rows, st);
 }
 
 }  // namespace
@@ -478,10 +511,12 @@ cudaError_t launch_reg_n(const MgStreamArgs &a, bool down, int64_t rows, cudaStr
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
     switch (a.n) {
-    case 127: return launch_reg_n<32>(a, down, rows, st);
-    case 255: return launch_reg_n<64>(a, down, rows, st);
-    case 511: return launch_reg_n<128>(a, down, rows, st);
-    case 1023: return launch_reg_n<256>(a, down, rows, st);
+    case 127: return launch_reg_n<4, 32, 1>(a, down, rows, st);
+    case 255: return launch_reg_n<8, 32, 1>(a, down, rows, st);
+    case 511: return launch_reg_n<8, 64, 1>(a, down, rows, st);
+    case 1023:
+        if (a.reg_ok == 2) return launch_reg_n<4, 256, 1>(a, down, rows, st);
+        return launch_reg_n<8, 128, 2>(a, down, rows, st);
     default: return cudaErrorNotSupported;
     }
 }
