@@ -45,6 +45,12 @@ HW_DEV void cp_async8z(void *smem, const void *gmem, bool valid)
                  "r"(valid ? 8 : 0));
 }
 
+HW_DEV void cp_async8s(unsigned saddr, const void *gmem)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
+}
+HW_DEV unsigned smem_u32(const void *p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 
 // shared-memory words (doubles) of one CTA.  Fine rows are staged whole
@@ -92,6 +98,12 @@ struct RegPass {
     double *Xg, *Bcg;
     double *bsm, *x0sm, *csm, *osm;
     double *HR, *HRes, *tot;              // [3][HS], [1][HS], [3][HS]
+    int cpo;                              // slot position of column tid (copy / flush lane)
+    int hoff;                             // slot position of the right-halo column P (t+1)
+    int ooff[P / 2];                      // slot positions of the own chunk's 16-byte pairs
+    int sb, sx;                           // ring slots of b(t) and x0(t+1) at step t
+    // column tid + k NT sits at cpo + k NT when the swizzle is periodic in NT
+    static constexpr bool LIN = (NT / 16) % (P / 2) == 0;
 
     // ---- register state ----
     double X1[2][P], X1L, X1R[2];          // sweep-1 rows (slot = row & 1) + halos
@@ -144,7 +156,13 @@ struct RegPass {
         HR = osm + SM::O;
         HRes = HR + 3 * HS;
         tot = HRes + HS;
-        for (int k = tid; k < SM::H; k += NT) HR[k] = 0.0;
+        for (int k = tid; k < SM::total; k += NT) sm[k] = 0.0;   // pads stay zero
+        cpo = phys(tid);
+        hoff = phys(P * (tid + 1));
+#pragma unroll
+        for (int h = 0; h < P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
+        sb = 4;                                // step -3 (the prologue's first group)
+        sx = 1;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
 #pragma unroll
@@ -169,40 +187,53 @@ struct RegPass {
         return DOWN ? (int64_t)i * n + j : (int64_t)(n - 1 - i) * n + (n - 1 - j);
     }
 
-    // cooperative zero-filling stage of fine row i (columns 0..n+1) of src
+    HW_DEV int koff(int k) const { return LIN ? k * NT : phys(tid + k * NT) - cpo; }
+
+    // cooperative coalesced stage of fine row i of src (columns 0..n-1; the
+    // pad columns n, n+1 are never written and stay zero).  Rows >= n: ZERO
+    // writes a zero row (x0 row n is the grid's zero boundary row), else the
+    // copy is skipped (such b / x0 rows only feed discarded sweeps).
+    template <bool ZERO>
     HW_DEV void stage_row(double *slot, const double *src, int i) const
     {
-        const bool vr = i < n;
-        const double *base = src + (vr ? gidx(i, 0) : 0);
+        if (i >= n) {
+            if constexpr (ZERO) {
 #pragma unroll
-        for (int k = 0; k < (P * NT + 2 + NT - 1) / NT; ++k) {
-            const int j = tid + k * NT;
-            if (j < P * NT + 2) {
-                const bool v = vr && j < n;
-                cp_async8z(slot + phys(j), base + (v ? gs * j : 0), v);
+                for (int k = 0; k < P; ++k) slot[cpo + koff(k)] = 0.0;
             }
+            return;
         }
+        const double *g = src + gidx(i, 0) + gs * tid;
+        const unsigned sa = smem_u32(slot + cpo);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (k < P - 1 || tid < NT - 1) cp_async8s(sa + 8u * koff(k), g + gs * k * NT);
     }
-    // coarse row ic, local columns -1..m at slot index J+1 (zeros outside)
+    // coarse row ic, local columns 0..m-1 at slot index J+1 (index 0 and m+1
+    // stay zero); rows -1 and m are zero rows
     HW_DEV void stage_coarse(int ic) const
     {
-        const bool vr = ic >= 0 && ic < m;
-        double *slot = csm + (size_t)ring(ic, SM::NCR) * CS;
-        const double *base = Xcg + (vr ? (int64_t)(m - 1 - ic) * m + (m - 1) : 0);
+        if (ic > m) return;
+        double *slot = csm + (size_t)ring(ic, SM::NCR) * CS + 1 + tid;
+        if (ic < 0 || ic == m) {
 #pragma unroll
-        for (int k = 0; k < (m + 2 + NT - 1) / NT; ++k) {
-            const int J = tid + k * NT - 1;
-            if (J <= m) {
-                const bool v = vr && J >= 0 && J < m;
-                cp_async8z(slot + J + 1, base - (v ? J : 0), v);
-            }
+            for (int k = 0; k < (m + NT - 1) / NT; ++k)
+                if (tid + k * NT < m) slot[k * NT] = 0.0;
+            return;
         }
+        const double *g = Xcg + (int64_t)(m - 1 - ic) * m + (m - 1) - tid;
+        const unsigned sa = smem_u32(slot);
+#pragma unroll
+        for (int k = 0; k < (m + NT - 1) / NT; ++k)
+            if (tid + k * NT < m) cp_async8s(sa + 8u * k * NT, g - k * NT);
     }
-    // the group step t issues: b(t+3), x0(t+4) and the coarse row x0(t+4) adds
+    HW_DEV int bslot(int back) const { return sb >= back ? sb - back : sb + SM::NB - back; }
+    // the group step t issues: b(t+3) (into b(t-4)'s slot), x0(t+4) (into
+    // x0(t+1)'s slot) and the coarse row x0(t+4) adds
     HW_DEV void issue(int t) const
     {
-        stage_row(bsm + (size_t)ring(t + 3, SM::NB) * RS, Bg, t + 3);
-        if constexpr (!(DOWN && ZS)) stage_row(x0sm + (size_t)ring(t + 4, SM::NX) * RS, Xg, t + 4);
+        stage_row<false>(bsm + (size_t)bslot(4) * RS, Bg, t + 3);
+        if constexpr (!(DOWN && ZS)) stage_row<true>(x0sm + (size_t)sx * RS, Xg, t + 4);
         if constexpr (!DOWN) {
             if (!((t + 4) & 1)) stage_coarse((t + 4) / 2);
         }
@@ -214,8 +245,7 @@ struct RegPass {
     {
 #pragma unroll
         for (int h = 0; h < P / 2; ++h) {
-            const int u = (P / 2) * tid + h;
-            const double2 w = *reinterpret_cast<const double2 *>(slot + ((u ^ ((u >> 3) & SWZ)) << 1));
+            const double2 w = *reinterpret_cast<const double2 *>(slot + ooff[h]);
             v[2 * h] = w.x;
             v[2 * h + 1] = w.y;
         }
@@ -224,11 +254,11 @@ struct RegPass {
     // x0 row i (P+1 values) from its slot; UP adds the prolongated coarse
     // correction (same arithmetic as mg2d_stream's prolongate)
     template <int IPAR, bool EDGE>
-    HW_DEV void load_x0(int i, double v[P + 1]) const
+    HW_DEV void load_x0(int i, int slotno, double v[P + 1]) const
     {
-        const double *slot = x0sm + (size_t)ring(i, SM::NX) * RS;
+        const double *slot = x0sm + (size_t)slotno * RS;
         load_chunk(slot, v);
-        v[P] = slot[phys(P * (tid + 1))];
+        v[P] = slot[hoff];
         if constexpr (!DOWN) {
             if (EDGE && i >= n) return;                  // row n stays a zero pad
             double ca[NC], cb[NC];
@@ -265,20 +295,21 @@ struct RegPass {
         }
     }
 
-    HW_DEV void load_b(int i, double b[P]) const
+    HW_DEV void load_b(int back, double b[P]) const
     {
-        load_chunk(bsm + (size_t)ring(i, SM::NB) * RS, b);
+        load_chunk(bsm + (size_t)bslot(back) * RS, b);
     }
 
     // coalesced copy of the staged output row (grid row i) to global memory
     HW_DEV void flush(int i) const
     {
-        double *dst = Xg + gidx(i, 0);
+        double *g = Xg + gidx(i, 0) + gs * tid;
+        double v[P];
 #pragma unroll
-        for (int k = 0; k < (n + NT - 1) / NT; ++k) {
-            const int j = tid + k * NT;
-            if (j < n) dst[gs * j] = osm[phys(j)];
-        }
+        for (int k = 0; k < P; ++k) v[k] = osm[cpo + koff(k)];
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (k < P - 1 || tid < NT - 1) g[gs * k * NT] = v[k];
     }
 
     // zero-carry chunk recurrence of one sweep over the thread's P points
@@ -332,16 +363,16 @@ struct RegPass {
             double z[P];
 #pragma unroll
             for (int k = 0; k < P; ++k) z[k] = 0.0;
-            load_b(t, b);
+            load_b(0, b);
             chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0]);
         } else {
-            load_x0<Q, EDGE>(t + 1, dn0);
-            load_b(t, b);
+            load_x0<Q, EDGE>(t + 1, sx, dn0);
+            load_b(0, b);
             chunk(X1[Q], X1L, X0n, X0n[P], dn0, dn0[P], b, y[0]);
         }
-        load_b(t - 2, b);
+        load_b(2, b);
         chunk(X2[Q], X2L, X1[PAR], X1R[PAR], X1[Q], X1R[Q], b, y[1]);
-        load_b(t - 4, b);
+        load_b(4, b);
         chunk(X3, X3L, X2[PAR], X2R[PAR], X2[Q], X2R[Q], b, y[2]);
 
         // residual of grid row t-6 from d(t-6), d(t-5)
@@ -438,14 +469,22 @@ struct RegPass {
                 }
             }
         }
+        advance();
+    }
+
+    HW_DEV void advance()
+    {
+        sb = sb + 1 == SM::NB ? 0 : sb + 1;
+        sx = sx + 1 == SM::NX ? 0 : sx + 1;
     }
 
     HW_DEV void run()
     {
         // prologue: x0 row 0 (+ coarse rows -1, 0), then the groups steps
         // -3..-1 would have issued
+        __syncthreads();                                 // zeroed slots before any copy lands
         if constexpr (!(DOWN && ZS)) {
-            stage_row(x0sm, Xg, 0);
+            stage_row<true>(x0sm, Xg, 0);
             if constexpr (!DOWN) {
                 stage_coarse(-1);
                 stage_coarse(0);
@@ -453,14 +492,17 @@ struct RegPass {
             cp_async_commit();
         }
         issue(-3);
+        advance();
         issue(-2);
+        advance();
         if constexpr (!(DOWN && ZS)) {
             cp_async_wait<2>();
             __syncthreads();
-            load_x0<0, true>(0, X0n);
+            load_x0<0, true>(0, 0, X0n);
             __syncthreads();                             // x0(3) reuses x0(0)'s slot
         }
         issue(-1);
+        advance();
         constexpr int nsteps = DOWN ? n + 6 : n + 5;     // the last flush is step n+4
         int t = 0;
         for (; t < 6; t += 2) {
