@@ -87,6 +87,90 @@ __global__ void wav_ana_stage(const double *__restrict__ X, int64_t x0, double *
     }
 }
 
+// ---------------------------------------------------------------------------
+// Whole-row stage kernels for the single-GPU transform: each thread owns one
+// column and a contiguous run of QP row pairs, so the input rows two
+// consecutive pairs share stay in registers and every input row is loaded
+// once per thread (the generic stage kernels above reload each one 2-3
+// times and launch one CTA per output row).  Same arithmetic per element.
+// ---------------------------------------------------------------------------
+constexpr int kWavQP = 16, kWavBS = 256;
+
+// synthesis stage j over the full prefix: pair q = fine nodes 2q, 2q+1
+__global__ void __launch_bounds__(kWavBS) wav_syn_pairs(const double *__restrict__ C,
+                                                        const double *__restrict__ Dm,
+                                                        double *__restrict__ Y, int j, double s,
+                                                        int64_t nx)
+{
+    const int nw = 1 << (j - 1);
+    const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
+    if (i >= nx) return;
+    const int q0 = blockIdx.y * kWavQP;
+    const int q1 = min(q0 + kWavQP, nw + 1);
+    double cq = C[(int64_t)q0 * nx + i];
+    double dm = q0 >= 1 ? Dm[(int64_t)(q0 - 1) * nx + i] : 0.0;   // d[q-1]
+#pragma unroll 4
+    for (int q = q0; q < q1; ++q) {
+        double acc = cq;
+        if (q >= 1) acc = add_rn(acc, mul_rn(qb(s, q - 1, nw), dm));
+        if (q < nw) {
+            const double dq = Dm[(int64_t)q * nx + i];
+            const double cn = C[(int64_t)(q + 1) * nx + i];
+            acc = add_rn(acc, mul_rn(qa(s, q), dq));
+            double od = mul_rn(0.5, cq);
+            od = add_rn(od, mul_rn(0.5, cn));
+            od = add_rn(od, mul_rn(s, dq));
+            Y[(int64_t)(2 * q + 1) * nx + i] = od;
+            cq = cn;
+            dm = dq;
+        }
+        Y[(int64_t)(2 * q) * nx + i] = acc;
+    }
+}
+
+// transposed stage j: pair r = coarse r (rows 2r-1..2r+1) and wavelet r
+// (rows 2r..2r+2)
+__global__ void __launch_bounds__(kWavBS) wav_ana_pairs(const double *__restrict__ X,
+                                                        double *__restrict__ Cout,
+                                                        double *__restrict__ Dout, int j,
+                                                        double s, int64_t nx)
+{
+    const int nw = 1 << (j - 1), nf = (1 << j) + 1;
+    const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
+    if (i >= nx) return;
+    const int r0 = blockIdx.y * kWavQP;
+    const int r1 = min(r0 + kWavQP, nw + 1);
+    double xm = r0 >= 1 ? X[(int64_t)(2 * r0 - 1) * nx + i] : 0.0;   // x[2r-1]
+    double x0 = X[(int64_t)(2 * r0) * nx + i];                      // x[2r]
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+        double acc;
+        if (r >= 1) {
+            acc = mul_rn(0.5, xm);
+            acc = add_rn(acc, x0);
+        } else {
+            acc = x0;
+        }
+        if (2 * r + 1 < nf) {
+            const double x1 = X[(int64_t)(2 * r + 1) * nx + i];
+            const double x2 = X[(int64_t)(2 * r + 2) * nx + i];
+            acc = add_rn(acc, mul_rn(0.5, x1));
+            double dd = mul_rn(qa(s, r), x0);
+            dd = add_rn(dd, mul_rn(s, x1));
+            dd = add_rn(dd, mul_rn(qb(s, r, nw), x2));
+            Dout[(int64_t)r * nx + i] = dd;
+            xm = x1;
+            x0 = x2;
+        }
+        Cout[(int64_t)r * nx + i] = acc;
+    }
+}
+
+static dim3 pair_grid(int pairs, int64_t nx)
+{
+    return dim3((unsigned)((nx + kWavBS - 1) / kWavBS), (unsigned)((pairs + kWavQP - 1) / kWavQP));
+}
+
 static dim3 stage_grid(int64_t rows, int64_t nx, int bs)
 {
     return dim3((unsigned)((nx + bs - 1) / bs), (unsigned)(rows < 65535 ? rows : 65535));
@@ -124,8 +208,9 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         for (int j = 1; j <= J; ++j) {
             double *dst = ((J - j) % 2 == 0) ? Y : S1;
             const int64_t nc = (1LL << (j - 1)) + 1;
-            cudaError_t e = launch_syn_stage(j, scale[j - 1], src, 0, X + nc * nx, 0, dst, 0,
-                                             (1LL << j) + 1, nx, st);
+            wav_syn_pairs<<<pair_grid((1 << (j - 1)) + 1, nx), kWavBS, 0, st>>>(
+                src, X + nc * nx, dst, j, scale[j - 1], nx);
+            cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
             ++*launches;
             src = dst;
@@ -135,8 +220,9 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         for (int j = J; j >= 1; --j) {
             double *cdst = (j == 1) ? Y : (((J - j) % 2 == 0) ? S1 : S2);
             const int64_t nc = (1LL << (j - 1)) + 1;
-            cudaError_t e = launch_ana_stage(j, scale[j - 1], src, 0, cdst, 0, nc, Y + nc * nx, 0,
-                                             1LL << (j - 1), nx, st);
+            wav_ana_pairs<<<pair_grid((1 << (j - 1)) + 1, nx), kWavBS, 0, st>>>(
+                src, cdst, Y + nc * nx, j, scale[j - 1], nx);
+            cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
             ++*launches;
             src = cdst;
