@@ -452,6 +452,7 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     if (const char *ev = getenv("HWG_MG_REG"))      // A/B switch for measurements
         if (ev[0] == '0') c->mg_reg_ok = 0;
         else if (ev[0] == '4' && c->mg_reg_ok) c->mg_reg_ok = 2;   // P = 4 at n = 1023
+        else if (ev[0] == '5' && c->mg_reg_ok) c->mg_reg_ok = 3;   // P = 4 for UP at n = 1023
     int rc;
 #define GO(x)                      \
     do {                           \

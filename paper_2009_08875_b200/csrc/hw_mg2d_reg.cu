@@ -102,6 +102,7 @@ struct RegPass {
     int hoff;                             // slot position of the right-halo column P (t+1)
     int ooff[P / 2];                      // slot positions of the own chunk's 16-byte pairs
     int sb, sx;                           // ring slots of b(t) and x0(t+1) at step t
+    int sc;                               // UP: ring slot of coarse row floor(t/2) at step t
     // column tid + k NT sits at cpo + k NT when the swizzle is periodic in NT
     static constexpr bool LIN = (NT / 16) % (P / 2) == 0;
 
@@ -163,6 +164,7 @@ struct RegPass {
         for (int h = 0; h < P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
         sb = 4;                                // step -3 (the prologue's first group)
         sx = 1;
+        sc = 0;                                // coarse row 0 at steps 0, 1
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
 #pragma unroll
@@ -177,9 +179,6 @@ struct RegPass {
 #pragma unroll
         for (int q2 = 0; q2 < P / 2; ++q2) acc[q2] = 0.0;
     }
-
-    // ring slot of row i (i >= -3)
-    static HW_DEV int ring(int i, int R) { return (i + 3 * R) % R; }
 
     // global element of (grid row i, local column j); UP is point-reversed
     static HW_DEV int64_t gidx(int i, int j)
@@ -211,10 +210,10 @@ struct RegPass {
     }
     // coarse row ic, local columns 0..m-1 at slot index J+1 (index 0 and m+1
     // stay zero); rows -1 and m are zero rows
-    HW_DEV void stage_coarse(int ic) const
+    HW_DEV void stage_coarse(int ic, int slotno) const
     {
         if (ic > m) return;
-        double *slot = csm + (size_t)ring(ic, SM::NCR) * CS + 1 + tid;
+        double *slot = csm + (size_t)slotno * CS + 1 + tid;
         if (ic < 0 || ic == m) {
 #pragma unroll
             for (int k = 0; k < (m + NT - 1) / NT; ++k)
@@ -234,8 +233,8 @@ struct RegPass {
     {
         stage_row<false>(bsm + (size_t)bslot(4) * RS, Bg, t + 3);
         if constexpr (!(DOWN && ZS)) stage_row<true>(x0sm + (size_t)sx * RS, Xg, t + 4);
-        if constexpr (!DOWN) {
-            if (!((t + 4) & 1)) stage_coarse((t + 4) / 2);
+        if constexpr (!DOWN) {        // coarse row floor(t/2) + 2 (even t)
+            if (!((t + 4) & 1)) stage_coarse((t + 4) / 2, sc + 2 >= SM::NCR ? sc + 2 - SM::NCR : sc + 2);
         }
         cp_async_commit();
     }
@@ -254,7 +253,7 @@ struct RegPass {
     // x0 row i (P+1 values) from its slot; UP adds the prolongated coarse
     // correction (same arithmetic as mg2d_stream's prolongate)
     template <int IPAR, bool EDGE>
-    HW_DEV void load_x0(int i, int slotno, double v[P + 1]) const
+    HW_DEV void load_x0(int i, int slotno, int cslot, double v[P + 1]) const
     {
         const double *slot = x0sm + (size_t)slotno * RS;
         load_chunk(slot, v);
@@ -262,8 +261,9 @@ struct RegPass {
         if constexpr (!DOWN) {
             if (EDGE && i >= n) return;                  // row n stays a zero pad
             double ca[NC], cb[NC];
-            const int c_a = IPAR ? (i - 1) / 2 : i / 2 - 1;
-            const double *pa = csm + (size_t)ring(c_a, SM::NCR) * CS + (P / 2) * tid;
+            // coarse rows c_a = floor((i-1)/2) (= floor(t/2) at step t = i-1)
+            // and, for even i, c_a + 1; slot of c_a passed in by the caller
+            const double *pa = csm + (size_t)cslot * CS + (P / 2) * tid;
 #pragma unroll
             for (int q = 0; q < NC; q += 2) {
                 const double2 w = *reinterpret_cast<const double2 *>(pa + q);
@@ -271,7 +271,7 @@ struct RegPass {
                 ca[q + 1] = w.y;
             }
             if constexpr (!IPAR) {
-                const double *pb = csm + (size_t)ring(c_a + 1, SM::NCR) * CS + (P / 2) * tid;
+                const double *pb = csm + (size_t)(cslot + 1 == SM::NCR ? 0 : cslot + 1) * CS + (P / 2) * tid;
 #pragma unroll
                 for (int q = 0; q < NC; q += 2) {
                     const double2 w = *reinterpret_cast<const double2 *>(pb + q);
@@ -366,7 +366,7 @@ struct RegPass {
             load_b(0, b);
             chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0]);
         } else {
-            load_x0<Q, EDGE>(t + 1, sx, dn0);
+            load_x0<Q, EDGE>(t + 1, sx, sc, dn0);
             load_b(0, b);
             chunk(X1[Q], X1L, X0n, X0n[P], dn0, dn0[P], b, y[0]);
         }
@@ -470,6 +470,7 @@ struct RegPass {
             }
         }
         advance();
+        if (PAR) sc = sc + 1 == SM::NCR ? 0 : sc + 1;
     }
 
     HW_DEV void advance()
@@ -486,23 +487,25 @@ struct RegPass {
         if constexpr (!(DOWN && ZS)) {
             stage_row<true>(x0sm, Xg, 0);
             if constexpr (!DOWN) {
-                stage_coarse(-1);
-                stage_coarse(0);
+                stage_coarse(-1, SM::NCR - 1);
+                stage_coarse(0, 0);
             }
             cp_async_commit();
         }
         issue(-3);
         advance();
-        issue(-2);
+        sc = SM::NCR - 1;                                // coarse slot of row floor(-2/2) = -1
+        issue(-2);                                       // (stages coarse row 1)
         advance();
         if constexpr (!(DOWN && ZS)) {
             cp_async_wait<2>();
             __syncthreads();
-            load_x0<0, true>(0, 0, X0n);
+            load_x0<0, true>(0, 0, SM::NCR - 1, X0n);
             __syncthreads();                             // x0(3) reuses x0(0)'s slot
         }
         issue(-1);
         advance();
+        sc = 0;
         constexpr int nsteps = DOWN ? n + 6 : n + 5;     // the last flush is step n+4
         int t = 0;
         for (; t < 6; t += 2) {
@@ -557,7 +560,8 @@ cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cuda
     case 255: return launch_reg_n<8, 32, 1>(a, down, rows, st);
     case 511: return launch_reg_n<8, 64, 1>(a, down, rows, st);
     case 1023:
-        if (a.reg_ok == 2) return launch_reg_n<4, 256, 1>(a, down, rows, st);
+        // HWG_MG_REG=4: P = 4 for both passes; =5: P = 4 for UP only (A/B)
+        if (a.reg_ok == 2 || (a.reg_ok == 3 && !down)) return launch_reg_n<4, 256, 1>(a, down, rows, st);
         return launch_reg_n<8, 128, 2>(a, down, rows, st);
     default: return cudaErrorNotSupported;
     }
