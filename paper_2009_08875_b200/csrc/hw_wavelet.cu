@@ -6,7 +6,10 @@
 // stage is one launch over (stage rows) x N_x with coalesced access along
 // the spatial axis; each output value accumulates the same products in the
 // same (CSR column) order as the reference's temporal_apply, without FMA
-// contraction, so the transform is bit-identical to the reference.
+// contraction, so the transform is bit-identical to the reference.  A
+// thread owns one column and a contiguous run of row pairs, so consecutive
+// outputs share their inputs through registers and every input row is
+// loaded once per thread.
 //
 // Synthesis (W): stage j maps the coarse nodal prefix c (rows 0..2^(j-1))
 // and the level-j wavelet coefficients d (rows 2^(j-1)+1..2^j, read from the
@@ -17,6 +20,8 @@
 #include "hw_common.cuh"
 #include "hw_internal.cuh"
 
+#include <algorithm>
+
 namespace hw {
 
 // a_k = -1 if k == 0 else -1/2 ; b_k = -1 if k == nw-1 else -1/2
@@ -24,75 +29,11 @@ namespace hw {
 __device__ __forceinline__ double qa(double s, int k) { return s * (k == 0 ? -1.0 : -0.5); }
 __device__ __forceinline__ double qb(double s, int k, int nw) { return s * (k == nw - 1 ? -1.0 : -0.5); }
 
-// Y[f - f0] <- (M_j [c ; d])[f] for fine nodes f in [f0, f0 + nf);
-// C[i - c0] = coarse node i, Dm[k - d0] = level-j wavelet k.
-// grid: (column blocks, output rows)
-__global__ void wav_syn_stage(const double *__restrict__ C, int64_t c0, const double *__restrict__ Dm,
-                              int64_t d0, double *__restrict__ Y, int64_t f0, int64_t nf, int j,
-                              double s, int64_t nx)
-{
-    const int nw = 1 << (j - 1);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nx) return;
-    for (int64_t rr = blockIdx.y; rr < nf; rr += gridDim.y) {
-        const int64_t r = f0 + rr;                 // global fine node
-        double acc;
-        if ((r & 1) == 0) {
-            const int q = (int)(r >> 1);           // coarse index
-            acc = C[(q - c0) * nx + i];            // P: 1.0 * c[q]
-            if (q >= 1)                            // Q col q-1: s * b_{q-1}
-                acc = add_rn(acc, mul_rn(qb(s, q - 1, nw), Dm[(q - 1 - d0) * nx + i]));
-            if (q < nw)                            // Q col q: s * a_q
-                acc = add_rn(acc, mul_rn(qa(s, q), Dm[(q - d0) * nx + i]));
-        } else {
-            const int k = (int)(r >> 1);
-            acc = mul_rn(0.5, C[(k - c0) * nx + i]);
-            acc = add_rn(acc, mul_rn(0.5, C[(k + 1 - c0) * nx + i]));
-            acc = add_rn(acc, mul_rn(s, Dm[(k - d0) * nx + i]));
-        }
-        Y[rr * nx + i] = acc;
-    }
-}
-
-// Cout[i - c0] = (P_j^T x)[i], i in [c0, c0 + nc); Dout[k - d0] = (Q_j^T x)[k],
-// k in [d0, d0 + nd); X[f - x0] = fine node f.  grid rows: nc + nd
-__global__ void wav_ana_stage(const double *__restrict__ X, int64_t x0, double *__restrict__ Cout,
-                              int64_t c0, int64_t nc, double *__restrict__ Dout, int64_t d0,
-                              int64_t nd, int j, double s, int64_t nx)
-{
-    const int nf = (1 << j) + 1, nw = 1 << (j - 1);
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nx) return;
-    auto xr = [&](int64_t f) { return X[(f - x0) * nx + i]; };
-    for (int64_t rr = blockIdx.y; rr < nc + nd; rr += gridDim.y) {
-        if (rr < nc) {
-            const int64_t r = c0 + rr;             // column r of P_j: rows 2r-1 (1/2), 2r (1), 2r+1 (1/2)
-            double acc;
-            if (r >= 1) {
-                acc = mul_rn(0.5, xr(2 * r - 1));
-                acc = add_rn(acc, xr(2 * r));
-            } else {
-                acc = xr(0);
-            }
-            if (2 * r + 1 < nf) acc = add_rn(acc, mul_rn(0.5, xr(2 * r + 1)));
-            Cout[rr * nx + i] = acc;
-        } else {
-            const int64_t kk = rr - nc;
-            const int k = (int)(d0 + kk);           // column k of Q_j: rows 2k, 2k+1, 2k+2
-            double acc = mul_rn(qa(s, k), xr(2 * k));
-            acc = add_rn(acc, mul_rn(s, xr(2 * k + 1)));
-            acc = add_rn(acc, mul_rn(qb(s, k, nw), xr(2 * k + 2)));
-            Dout[kk * nx + i] = acc;
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
-// Whole-row stage kernels for the single-GPU transform: each thread owns one
-// column and a contiguous run of QP row pairs, so the input rows two
-// consecutive pairs share stay in registers and every input row is loaded
-// once per thread (the generic stage kernels above reload each one 2-3
-// times and launch one CTA per output row).  Same arithmetic per element.
+// Full-prefix stage kernels of the single-GPU transform: each thread owns
+// one column and a contiguous run of QP row pairs (per-element kernels that
+// reload every input 2-3 times and launch one CTA per output row took 1.9x
+// as long at J = 10).
 // ---------------------------------------------------------------------------
 constexpr int kWavQP = 16, kWavBS = 256;
 
@@ -171,16 +112,111 @@ static dim3 pair_grid(int pairs, int64_t nx)
     return dim3((unsigned)((nx + kWavBS - 1) / kWavBS), (unsigned)((pairs + kWavQP - 1) / kWavQP));
 }
 
-static dim3 stage_grid(int64_t rows, int64_t nx, int bs)
+// ---- general windows (the time-slab entries hwg_syn_stage / hwg_ana_stage):
+// the same per-thread runs of pairs, every load guarded by what the in-range
+// outputs need, register carries tracked with validity flags.
+
+// Y[f - f0] <- (M_j [c ; d])[f], f in [f0, f0 + nf); C[i - c0], Dm[k - d0]
+__global__ void __launch_bounds__(kWavBS) wav_syn_window(const double *__restrict__ C, int64_t c0,
+                                                         const double *__restrict__ Dm, int64_t d0,
+                                                         double *__restrict__ Y, int64_t f0,
+                                                         int64_t nf, int j, double s, int64_t nx)
 {
-    return dim3((unsigned)((nx + bs - 1) / bs), (unsigned)(rows < 65535 ? rows : 65535));
+    const int nw = 1 << (j - 1);
+    const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
+    if (i >= nx) return;
+    const int64_t qlo = f0 >> 1, qhi = (f0 + nf - 1) >> 1;       // pairs touched
+    const int64_t q0 = qlo + (int64_t)blockIdx.y * kWavQP;
+    const int64_t q1 = q0 + kWavQP - 1 < qhi ? q0 + kWavQP - 1 : qhi;
+    auto cr = [&](int64_t q) { return C[(q - c0) * nx + i]; };
+    auto dr = [&](int64_t k) { return Dm[(k - d0) * nx + i]; };
+    double cq = 0.0, dm = 0.0;
+    bool have_c = false, have_d = false;
+    for (int64_t q = q0; q <= q1; ++q) {
+        const bool ne = 2 * q >= f0 && 2 * q < f0 + nf;
+        const bool no = q < nw && 2 * q + 1 >= f0 && 2 * q + 1 < f0 + nf;
+        if (!have_c) cq = cr(q);
+        if (ne && q >= 1 && !have_d) dm = dr(q - 1);
+        const bool ldq = (ne && q < nw) || no;
+        const double dq = ldq ? dr(q) : 0.0;
+        if (ne) {
+            double acc = cq;
+            if (q >= 1) acc = add_rn(acc, mul_rn(qb(s, (int)q - 1, nw), dm));
+            if (q < nw) acc = add_rn(acc, mul_rn(qa(s, (int)q), dq));
+            Y[(2 * q - f0) * nx + i] = acc;
+        }
+        if (no) {
+            const double cn = cr(q + 1);
+            double od = mul_rn(0.5, cq);
+            od = add_rn(od, mul_rn(0.5, cn));
+            od = add_rn(od, mul_rn(s, dq));
+            Y[(2 * q + 1 - f0) * nx + i] = od;
+            cq = cn;
+        }
+        have_c = no;
+        dm = dq;
+        have_d = ldq;
+    }
+}
+
+// Cout[r - c0] = (P_j^T x)[r], r in [c0, c0 + nc); Dout[k - d0] = (Q_j^T x)[k],
+// k in [d0, d0 + nd); X[f - x0] = fine node f
+__global__ void __launch_bounds__(kWavBS) wav_ana_window(const double *__restrict__ X, int64_t x0,
+                                                         double *__restrict__ Cout, int64_t c0,
+                                                         int64_t nc, double *__restrict__ Dout,
+                                                         int64_t d0, int64_t nd, int j, double s,
+                                                         int64_t nx)
+{
+    const int nw = 1 << (j - 1), nf = (1 << j) + 1;
+    const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
+    if (i >= nx) return;
+    const int64_t lo = nc && nd ? (c0 < d0 ? c0 : d0) : (nc ? c0 : d0);
+    const int64_t hi = nc && nd ? (c0 + nc > d0 + nd ? c0 + nc : d0 + nd) : (nc ? c0 + nc : d0 + nd);
+    const int64_t r0 = lo + (int64_t)blockIdx.y * kWavQP;
+    const int64_t r1 = r0 + kWavQP < hi ? r0 + kWavQP : hi;
+    auto xr = [&](int64_t f) { return X[(f - x0) * nx + i]; };
+    double xm = 0.0, xa = 0.0;                          // x[2r-1], x[2r]
+    bool have_m = false, have_a = false;
+    for (int64_t r = r0; r < r1; ++r) {
+        const bool cin = r >= c0 && r < c0 + nc;
+        const bool din = r >= d0 && r < d0 + nd;
+        if (!have_a) xa = xr(2 * r);
+        const bool l1 = (cin && 2 * r + 1 < nf) || din;
+        const double x1 = l1 ? xr(2 * r + 1) : 0.0;
+        if (cin) {
+            double acc;
+            if (r >= 1) {
+                if (!have_m) xm = xr(2 * r - 1);
+                acc = mul_rn(0.5, xm);
+                acc = add_rn(acc, xa);
+            } else {
+                acc = xa;
+            }
+            if (2 * r + 1 < nf) acc = add_rn(acc, mul_rn(0.5, x1));
+            Cout[(r - c0) * nx + i] = acc;
+        }
+        double x2 = 0.0;
+        if (din) {
+            x2 = xr(2 * r + 2);
+            double dd = mul_rn(qa(s, (int)r), xa);
+            dd = add_rn(dd, mul_rn(s, x1));
+            dd = add_rn(dd, mul_rn(qb(s, (int)r, nw), x2));
+            Dout[(r - d0) * nx + i] = dd;
+        }
+        xm = x1;
+        have_m = l1;
+        xa = x2;
+        have_a = din;
+    }
 }
 
 cudaError_t launch_syn_stage(int j, double s, const double *C, int64_t c0, const double *Dm,
                              int64_t d0, double *Y, int64_t f0, int64_t nf, int64_t nx,
                              cudaStream_t st)
 {
-    wav_syn_stage<<<stage_grid(nf, nx, 256), 256, 0, st>>>(C, c0, Dm, d0, Y, f0, nf, j, s, nx);
+    if (nf <= 0) return cudaSuccess;
+    const int64_t pairs = ((f0 + nf - 1) >> 1) - (f0 >> 1) + 1;
+    wav_syn_window<<<pair_grid((int)pairs, nx), kWavBS, 0, st>>>(C, c0, Dm, d0, Y, f0, nf, j, s, nx);
     return cudaGetLastError();
 }
 
@@ -188,8 +224,11 @@ cudaError_t launch_ana_stage(int j, double s, const double *X, int64_t x0, doubl
                              int64_t nc, double *Dm, int64_t d0, int64_t nd, int64_t nx,
                              cudaStream_t st)
 {
-    wav_ana_stage<<<stage_grid(nc + nd, nx, 256), 256, 0, st>>>(X, x0, C, c0, nc, Dm, d0, nd, j,
-                                                                  s, nx);
+    if (nc + nd <= 0) return cudaSuccess;
+    const int64_t lo = nc && nd ? std::min(c0, d0) : (nc ? c0 : d0);
+    const int64_t hi = nc && nd ? std::max(c0 + nc, d0 + nd) : (nc ? c0 + nc : d0 + nd);
+    wav_ana_window<<<pair_grid((int)(hi - lo), nx), kWavBS, 0, st>>>(X, x0, C, c0, nc, Dm, d0, nd,
+                                                                     j, s, nx);
     return cudaGetLastError();
 }
 

@@ -132,3 +132,23 @@ def test_no_oracle_import_in_product():
     for path in glob.glob(os.path.join(ROOT, "paper_2009_08875_b200", "**", "*.py"), recursive=True):
         src = open(path).read()
         assert "oracle" not in src.replace("oracle/", ""), path
+
+
+def test_library_has_no_undefined_internal_symbols():
+    """Every hw:: function the translation units reference is defined in the
+    shared library (a missing definition would only fail at dlopen on the
+    GPU box)."""
+    import shutil
+    import subprocess
+
+    from paper_2009_08875_b200 import _lib
+
+    so = _lib.library_path() if hasattr(_lib, "library_path") else None
+    if so is None:
+        import paper_2009_08875_b200 as pkg
+        so = os.path.join(os.path.dirname(pkg.__file__), "libhwgpu.so")
+    if not os.path.exists(so) or shutil.which("nm") is None:
+        pytest.skip("library not built / nm missing")
+    out = subprocess.run(["nm", "-D", "--undefined-only", so], capture_output=True, text=True).stdout
+    missing = [ln.split()[-1] for ln in out.splitlines() if "_ZN2hw" in ln]
+    assert not missing, missing
