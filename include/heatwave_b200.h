@@ -230,6 +230,13 @@ int hwg_temporal_rows(hwg_ctx *ctx, int band, const double *X, int64_t x0, doubl
 int hwg_mg_rows_dev(hwg_ctx *ctx, const int32_t *ops, const double *B, double *X, int64_t rows,
                     void *stream);
 
+/* hwg_mg_rows_dev plus the per-row partials part[r] = <Y row r, X row r> of
+ * the result, fused into the last multigrid pass (the PCG's r.z after
+ * z = K_X r; solver.py:233-236).  Deterministic; the same kernels on every
+ * rank, so time slabs reproduce the single-GPU partials bit for bit. */
+int hwg_mg_rows_dev_dot(hwg_ctx *ctx, const int32_t *ops, const double *B, double *X,
+                        int64_t rows, const double *Y, double *part, void *stream);
+
 /* Per-row partial inner products part[r] = sum_i X[r,i] Y[r,i] (device). */
 int hwg_row_partials(hwg_ctx *ctx, const double *X, const double *Y, int64_t rows, double *part,
                      void *stream);

@@ -278,9 +278,18 @@ static int64_t level_size(const hwg_ctx *c, int l)
 }
 
 // X[r] = MG_op(B[r]) for rows [0, rows); row_op: device per-row operator or null
-static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op,
-                    const int32_t *row_op, cudaStream_t st)
+// dot_y (optional): also dot_part[r] = <dot_y row r, X row r>, fused into the
+// last finest-level UP pass when that pass runs on mg2d_reg, else by row_dots
+static bool mg_dot_fusable(const hwg_ctx *c)
 {
+    return c->dim == 2 && c->K >= 7 && c->K <= 10 && c->mg_reg_ok;
+}
+
+static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op,
+                    const int32_t *row_op, cudaStream_t st, const double *dot_y = nullptr,
+                    double *dot_part = nullptr)
+{
+    const bool fuse = dot_y && mg_dot_fusable(c);
     for (int64_t r0 = 0; r0 < rows; r0 += c->rows_max) {
         const int64_t nr = std::min<int64_t>(c->rows_max, rows - r0);
         const double *Bp = B + r0 * c->nx;
@@ -346,12 +355,20 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.row_op = ro;
                 a.op = op;
                 a.reg_ok = c->mg_reg_ok;
+                if (fuse && l == c->K && cyc == c->nv - 1) {
+                    a.dot_y = dot_y + r0 * c->nx;
+                    a.dot_part = dot_part + r0;
+                }
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
                 ProfScope ps(c, st, l == c->K ? 1 : 3, 8.0 * nr * (3 * n2 + m2));
                 CK(mg2d_stream_launch(a, false, nr, st));
                 ++c->launches;
             }
         }
+    }
+    if (dot_y && !fuse) {
+        CK(launch_row_partials(dot_y, X, rows, c->nx, dot_part, st));
+        ++c->launches;
     }
     return HWG_OK;
 }
@@ -380,13 +397,15 @@ static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
     return HWG_OK;
 }
 
-// K_X = blockdiag[C_l A_x C_l] (system.py:242-276)
-static int kx(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
+// K_X = blockdiag[C_l A_x C_l] (system.py:242-276); dot_y (optional): also
+// the per-row partials of <dot_y, Y>, fused into the last multigrid pass
+static int kx(hwg_ctx *c, const double *X, double *Y, cudaStream_t st,
+              const double *dot_y = nullptr, double *dot_part = nullptr)
 {
     TRY(mg_apply(c, X, Y, c->nt, 0, c->row_op_kx, st));
     CK(launch_stencil_rows(Y, nullptr, c->G12, c->grid, c->SM, c->SA, c->nt, st));
     ++c->launches;
-    TRY(mg_apply(c, c->G12, Y, c->nt, 0, c->row_op_kx, st));
+    TRY(mg_apply(c, c->G12, Y, c->nt, 0, c->row_op_kx, st, dot_y, dot_part));
     return HWG_OK;
 }
 
@@ -408,7 +427,7 @@ static int ensure_pcg(hwg_ctx *c)
 extern "C" {
 
 const char *hwg_last_error(void) { return g_err.c_str(); }
-int hwg_version(void) { return 2; }
+int hwg_version(void) { return 3; }
 
 int hwg_create(const hwg_desc *desc, hwg_ctx **out)
 {
@@ -684,9 +703,10 @@ int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
     }
     CK(cudaMemcpyAsync(c->r, f, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
     CK(cudaEventRecord(ev[1], st));
-    TRY(kx(c, c->r, c->z, st));
+    TRY(kx(c, c->r, c->z, st, c->r, c->part));           // r.z fused into K_X's last pass
     CK(cudaEventRecord(ev[2], st));
-    CK(launch_dot(c->r, c->z, nt, nx, c->part, c->tmp, c->scal + 0, st, &c->launches));
+    CK(launch_tree(c->part, nt, c->tmp, c->scal + 0, st));
+    ++c->launches;
     CK(cudaMemcpyAsync(c->hscal, c->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     float ms = 0.f;
@@ -720,9 +740,10 @@ int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
             ++c->launches;
         }
         CK(cudaEventRecord(ev[4], st));
-        TRY(kx(c, c->r, c->z, st));
+        TRY(kx(c, c->r, c->z, st, c->r, c->part));       // r.z fused into K_X's last pass
         CK(cudaEventRecord(ev[5], st));
-        CK(launch_dot(c->r, c->z, nt, nx, c->part, c->tmp, c->scal + 2, st, &c->launches));
+        CK(launch_tree(c->part, nt, c->tmp, c->scal + 2, st));
+        ++c->launches;
         CK(cudaMemcpyAsync(c->hscal + 1, c->scal + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(launch_pcg_beta(c->scal, st));
         CK(launch_update_p(c->p, c->z, c->scal, N, st));
@@ -838,6 +859,15 @@ int hwg_mg_rows_dev(hwg_ctx *c, const int32_t *ops, const double *B, double *X, 
     if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
     if (rows == 0) return HWG_OK;
     return mg_apply(c, B, X, rows, 0, ops, S(stream));
+}
+
+int hwg_mg_rows_dev_dot(hwg_ctx *c, const int32_t *ops, const double *B, double *X, int64_t rows,
+                        const double *Y, double *part, void *stream)
+{
+    if (!c || !ops || !B || !X || !Y || !part || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
+    if (rows == 0) return HWG_OK;
+    return mg_apply(c, B, X, rows, 0, ops, S(stream), Y, part);
 }
 
 int hwg_row_partials(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *part,

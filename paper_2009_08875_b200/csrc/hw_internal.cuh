@@ -21,6 +21,8 @@ struct MgStreamArgs {
     int op;                             // default operator
     int zero_start;                     // DOWN: iterate starts at zero
     int reg_ok;                         // |beta| small enough for mg2d_reg
+    const double *dot_y;                // UP (mg2d_reg): dot_part[row] = <dot_y row, final X row>
+    double *dot_part;
 };
 
 struct MgCoarseArgs {

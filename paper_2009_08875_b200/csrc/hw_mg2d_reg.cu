@@ -96,6 +96,8 @@ struct RegPass {
     double gl;                            // gamma^lane
     const double *Bg, *Xcg;               // row 0 of this temporal row's level arrays
     double *Xg, *Bcg;
+    const double *Dg;                     // UP: fused inner-product operand (or null)
+    double dsum;                          //     this thread's share of <Dg, X>
     double *bsm, *x0sm, *csm, *osm;
     double *HR, *HRes, *tot;              // [3][HS], [1][HS], [3][HS]
     int cpo;                              // slot position of column tid (copy / flush lane)
@@ -150,6 +152,8 @@ struct RegPass {
         Xg = a.X + row * a.ldX;
         Xcg = DOWN ? nullptr : a.Xc + row * a.ldXc;
         Bcg = DOWN ? a.Bc + row * a.ldBc + (P / 2) * tid : nullptr;
+        Dg = (!DOWN && a.dot_y) ? a.dot_y + row * a.ldX : nullptr;
+        dsum = 0.0;
         bsm = sm;
         x0sm = bsm + SM::B;
         csm = x0sm + SM::X0;
@@ -301,7 +305,7 @@ struct RegPass {
     }
 
     // coalesced copy of the staged output row (grid row i) to global memory
-    HW_DEV void flush(int i) const
+    HW_DEV void flush(int i)
     {
         double *g = Xg + gidx(i, 0) + gs * tid;
         double v[P];
@@ -310,6 +314,31 @@ struct RegPass {
 #pragma unroll
         for (int k = 0; k < P; ++k)
             if (k < P - 1 || tid < NT - 1) g[gs * k * NT] = v[k];
+        if (!DOWN && Dg) {                       // fused inner product, fixed order
+            const double *d = Dg + gidx(i, 0) + gs * tid;
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+                if (k < P - 1 || tid < NT - 1) dsum = fma(d[gs * k * NT], v[k], dsum);
+        }
+    }
+
+    // per-row partial of the fused inner product: xor-butterfly in each warp,
+    // then the warp totals in warp order (deterministic)
+    HW_DEV void finish_dot(const MgStreamArgs &a)
+    {
+        if (DOWN || !Dg) return;
+        double v = dsum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if (lane == 0) tot[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            double u = lane < NW ? tot[lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+            if (lane == 0) a.dot_part[blockIdx.x] = u;
+        }
     }
 
     // zero-carry chunk recurrence of one sweep over the thread's P points
@@ -530,6 +559,7 @@ __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
     extern __shared__ __align__(16) double sm[];
     RegPass<P, NT, DOWN, ZS> p(a, sm);
     p.run();
+    p.finish_dot(a);
 }
 
 template <int P, int NT, bool DOWN, bool ZS, int MINB>

@@ -142,6 +142,11 @@ class GpuContext:
         _lib.check(self.lib.hwg_mg_rows_dev(self.handle, ptr(ops), ptr(B), ptr(X), B.shape[0],
                                             self.stream()))
 
+    def mg_rows_dev_dot(self, ops, B, X, Y, part):
+        """X = MG(B) row-wise and part[r] = <Y[r], X[r]> (fused when possible)."""
+        _lib.check(self.lib.hwg_mg_rows_dev_dot(self.handle, ptr(ops), ptr(B), ptr(X), B.shape[0],
+                                                ptr(Y), ptr(part), self.stream()))
+
     def row_partials(self, X, Y, part):
         _lib.check(self.lib.hwg_row_partials(self.handle, ptr(X), ptr(Y), X.shape[0], ptr(part),
                                              self.stream()))

@@ -331,13 +331,26 @@ class SlabSystem:
             st.k.spatial(1, y, st.mid)
             st.k.mg_rows_dev(st.ops_kx, st.mid, y)
 
+    def kx_dot(self, X, Y):
+        """Y = K_X X and <X, Y>, the per-row partials fused into the last
+        multigrid pass (the same kernels as the single-GPU hwg_pcg)."""
+        for st, x, y in zip(self.states, X, Y):
+            st.k.mg_rows_dev(st.ops_kx, x, y)
+            st.k.spatial(1, y, st.mid)
+            st.k.mg_rows_dev_dot(st.ops_kx, st.mid, y, x, st.part)
+        return self._reduce_partials()
+
     def dot(self, X, Y):
         """Inner product with the reference's fixed tree over the per-row
         partials in GLOBAL row order (solver.py:111-129) -- identical for
         every number of ranks."""
-        contrib = []
         for st, x, y in zip(self.states, X, Y):
             st.k.row_partials(x, y, st.part)
+        return self._reduce_partials()
+
+    def _reduce_partials(self):
+        contrib = []
+        for st in self.states:
             contrib.append(st.part * st.owned)
         gathered = self.comm.allgather(self.states, contrib)
         vals = []
@@ -386,8 +399,7 @@ def pcg(system: SlabSystem, F, W, epsilon=0.0, rtol=0.0, max_iterations=200,
         w.zero_()
     if system.dot(F, F) == 0.0:
         return SlabPCGResult(0, [0.0])
-    system.kx(R, Z)
-    rho = system.dot(R, Z)
+    rho = system.kx_dot(R, Z)
     hist = [math.sqrt(max(rho, 0.0))]
     eps = rtol * hist[0] if rtol > 0 else epsilon
     if rho <= eps ** 2:
@@ -409,8 +421,7 @@ def pcg(system: SlabSystem, F, W, epsilon=0.0, rtol=0.0, max_iterations=200,
             system.axpy(-1.0, Z, R)
         else:
             system.axpy(-alpha, Q, R)
-        system.kx(R, Z)
-        rho_new = system.dot(R, Z)
+        rho_new = system.kx_dot(R, Z)
         beta = rho_new / rho
         alphas.append(alpha)
         betas.append(beta)
@@ -440,6 +451,7 @@ class CudaKernels:
         self.bside_rows = ctx.bside_rows
         self.bt_rows = ctx.bt_rows
         self.mg_rows_dev = ctx.mg_rows_dev
+        self.mg_rows_dev_dot = ctx.mg_rows_dev_dot
         self.row_partials = ctx.row_partials
         self.tree_sum = ctx.tree_sum
         self.axpy = ctx.axpy

@@ -92,6 +92,10 @@ class NumpyKernels:
         _np(Y)[:] = O.spatial(A, np.ascontiguousarray(_np(X)), np.empty(tuple(X.shape)))
 
     # --- vectors -----------------------------------------------------------
+    def mg_rows_dev_dot(self, ops, B, X, Y, part):
+        self.mg_rows_dev(ops, B, X)
+        self.row_partials(Y, X, part)
+
     def row_partials(self, X, Y, part):
         x, y = np.ascontiguousarray(_np(X)), np.ascontiguousarray(_np(Y))
         p = np.empty(x.shape[0])

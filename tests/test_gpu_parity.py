@@ -237,3 +237,29 @@ def test_register_mg_matches_streamed(K, alpha, mu, monkeypatch):
         outs.append(X)
     assert np.isfinite(outs[0]).all()
     assert relative_diff(outs[0], outs[1]) <= 1e-12 * 4.0 ** max(0, K - 8)
+
+
+@pytest.mark.parametrize("K", [6, 7, 9, 10])
+def test_mg_rows_fused_inner_product(K):
+    """hwg_mg_rows_dev_dot: X = MG(B) exactly as hwg_mg_rows_dev, and the
+    per-row partials <Y, X> (fused into the last finest-level UP pass for
+    K >= 7, row_dots otherwise) agree with a separate row_dots up to
+    summation order."""
+    from paper_2009_08875_b200.device import GpuContext
+
+    ctx = GpuContext(2, 3, K)
+    rows, nx = 2 * ctx.n_t, ctx.n_x
+    gen = torch.Generator(device="cuda").manual_seed(K)
+    B = torch.randn((rows, nx), dtype=torch.float64, device="cuda", generator=gen)
+    Y = torch.randn((rows, nx), dtype=torch.float64, device="cuda", generator=gen)
+    ops = torch.zeros(rows, dtype=torch.int32, device="cuda")
+    X1, X2 = torch.empty_like(B), torch.empty_like(B)
+    p1 = torch.empty(rows, dtype=torch.float64, device="cuda")
+    p2 = torch.empty_like(p1)
+    ctx.mg_rows_dev(ops, B, X1)
+    ctx.mg_rows_dev_dot(ops, B, X2, Y, p2)
+    ctx.row_partials(Y, X1, p1)
+    torch.cuda.synchronize()
+    assert torch.equal(X1, X2)
+    scale = (Y.abs() * X1.abs()).sum(dim=1)
+    assert float(((p1 - p2).abs() / scale).max()) <= 1e-14
