@@ -105,6 +105,7 @@ struct RegPass {
     int ooff[P / 2];                      // slot positions of the own chunk's 16-byte pairs
     int sb, sx;                           // ring slots of b(t) and x0(t+1) at step t
     int sc;                               // UP: ring slot of coarse row floor(t/2) at step t
+    double HC[NC];                        // UP: 0.5 x the latest coarse row this thread reads
     // column tid + k NT sits at cpo + k NT when the swizzle is periodic in NT
     static constexpr bool LIN = (NT / 16) % (P / 2) == 0;
 
@@ -122,6 +123,15 @@ struct RegPass {
     {
         const int u = j >> 1;
         return ((u ^ ((u >> 3) & SWZ)) << 1) | (j & 1);
+    }
+
+    // coarse slot position of index x (= local coarse column + 1): 16-byte
+    // units XOR-swizzled by bit 3 so a thread's LDS.128 of its NC values
+    // (units (P/4) t .. ) are bank-conflict free
+    static HW_DEV int cphys(int x)
+    {
+        const int u = x >> 1;
+        return ((u ^ ((u >> 3) & 1)) << 1) | (x & 1);
     }
 
     HW_DEV RegPass(const MgStreamArgs &a, double *sm)
@@ -182,6 +192,8 @@ struct RegPass {
         for (int e = 0; e <= P; ++e) X0n[e] = 0.0;
 #pragma unroll
         for (int q2 = 0; q2 < P / 2; ++q2) acc[q2] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) HC[q] = 0.0;          // coarse row -1
     }
 
     // global element of (grid row i, local column j); UP is point-reversed
@@ -217,7 +229,8 @@ struct RegPass {
     HW_DEV void stage_coarse(int ic, int slotno) const
     {
         if (ic > m) return;
-        double *slot = csm + (size_t)slotno * CS + 1 + tid;
+        static_assert((NT / 16) % 2 == 0, "coarse swizzle periodic in NT");
+        double *slot = csm + (size_t)slotno * CS + cphys(1 + tid);
         if (ic < 0 || ic == m) {
 #pragma unroll
             for (int k = 0; k < (m + NT - 1) / NT; ++k)
@@ -233,13 +246,13 @@ struct RegPass {
     HW_DEV int bslot(int back) const { return sb >= back ? sb - back : sb + SM::NB - back; }
     // the group step t issues: b(t+3) (into b(t-4)'s slot), x0(t+4) (into
     // x0(t+1)'s slot) and the coarse row x0(t+4) adds
+    template <int TPAR>                // TPAR = t & 1
     HW_DEV void issue(int t) const
     {
         stage_row<false>(bsm + (size_t)bslot(4) * RS, Bg, t + 3);
         if constexpr (!(DOWN && ZS)) stage_row<true>(x0sm + (size_t)sx * RS, Xg, t + 4);
-        if constexpr (!DOWN) {        // coarse row floor(t/2) + 2 (even t)
-            if (!((t + 4) & 1)) stage_coarse((t + 4) / 2, sc + 2 >= SM::NCR ? sc + 2 - SM::NCR : sc + 2);
-        }
+        if constexpr (!DOWN && TPAR == 0)    // coarse row floor(t/2) + 2 (even t)
+            stage_coarse((t + 4) / 2, sc + 2 >= SM::NCR ? sc + 2 - SM::NCR : sc + 2);
         cp_async_commit();
     }
 
@@ -257,30 +270,26 @@ struct RegPass {
     // x0 row i (P+1 values) from its slot; UP adds the prolongated coarse
     // correction (same arithmetic as mg2d_stream's prolongate)
     template <int IPAR, bool EDGE>
-    HW_DEV void load_x0(int i, int slotno, int cslot, double v[P + 1]) const
+    HW_DEV void load_x0(int i, int slotno, int cslot, double v[P + 1])
     {
         const double *slot = x0sm + (size_t)slotno * RS;
         load_chunk(slot, v);
         v[P] = slot[hoff];
         if constexpr (!DOWN) {
             if (EDGE && i >= n) return;                  // row n stays a zero pad
-            double ca[NC], cb[NC];
-            // coarse rows c_a = floor((i-1)/2) (= floor(t/2) at step t = i-1)
-            // and, for even i, c_a + 1; slot of c_a passed in by the caller
-            const double *pa = csm + (size_t)cslot * CS + (P / 2) * tid;
-#pragma unroll
-            for (int q = 0; q < NC; q += 2) {
-                const double2 w = *reinterpret_cast<const double2 *>(pa + q);
-                ca[q] = w.x;
-                ca[q + 1] = w.y;
-            }
+            // coarse rows c_a = floor((i-1)/2) and, for even i, c_a + 1.  Row
+            // c_a is the one the previous step loaded (kept as exact halves in
+            // HC), so each pair of steps reads one new coarse row.  0.5 c is
+            // exact, hence h_a + h_b == 0.5 c_a + 0.5 c_b and h + h == c:
+            // the same rounding as the stream kernel's prolongation.
+            double hb[NC];
             if constexpr (!IPAR) {
-                const double *pb = csm + (size_t)(cslot + 1 == SM::NCR ? 0 : cslot + 1) * CS + (P / 2) * tid;
+                const double *pb = csm + (size_t)(cslot + 1 == SM::NCR ? 0 : cslot + 1) * CS;
 #pragma unroll
                 for (int q = 0; q < NC; q += 2) {
-                    const double2 w = *reinterpret_cast<const double2 *>(pb + q);
-                    cb[q] = w.x;
-                    cb[q + 1] = w.y;
+                    const double2 w = *reinterpret_cast<const double2 *>(pb + cphys((P / 2) * tid + q));
+                    hb[q] = 0.5 * w.x;
+                    hb[q + 1] = 0.5 * w.y;
                 }
             }
 #pragma unroll
@@ -288,12 +297,16 @@ struct RegPass {
                 double pv;
                 if (e & 1) {
                     const int q = (e + 1) / 2;
-                    pv = IPAR ? ca[q] : 0.5 * ca[q] + 0.5 * cb[q];
+                    pv = IPAR ? HC[q] + HC[q] : HC[q] + hb[q];
                 } else {
                     const int q = e / 2;
-                    pv = IPAR ? 0.5 * ca[q] + 0.5 * ca[q + 1] : 0.5 * ca[q] + 0.5 * cb[q + 1];
+                    pv = IPAR ? HC[q] + HC[q + 1] : HC[q] + hb[q + 1];
                 }
                 v[e] = v[e] + pv;
+            }
+            if constexpr (!IPAR) {
+#pragma unroll
+                for (int q = 0; q < NC; ++q) HC[q] = hb[q];
             }
             if (last) v[P - 1] = v[P] = 0.0;             // columns n, n+1
         }
@@ -425,7 +438,7 @@ struct RegPass {
         }
         __syncthreads();                                 // (B) warp totals visible, output row
                                                          //     and the oldest ring slots free
-        issue(t);
+        issue<PAR>(t);
 
         // ---- phase B: carries, new rows, halos ----
         double xn[3][P], cin[3];
@@ -521,10 +534,10 @@ struct RegPass {
             }
             cp_async_commit();
         }
-        issue(-3);
+        issue<1>(-3);
         advance();
         sc = SM::NCR - 1;                                // coarse slot of row floor(-2/2) = -1
-        issue(-2);                                       // (stages coarse row 1)
+        issue<0>(-2);                                    // (stages coarse row 1)
         advance();
         if constexpr (!(DOWN && ZS)) {
             cp_async_wait<2>();
@@ -532,7 +545,7 @@ struct RegPass {
             load_x0<0, true>(0, 0, SM::NCR - 1, X0n);
             __syncthreads();                             // x0(3) reuses x0(0)'s slot
         }
-        issue(-1);
+        issue<1>(-1);
         advance();
         sc = 0;
         constexpr int nsteps = DOWN ? n + 6 : n + 5;     // the last flush is step n+4
