@@ -425,35 +425,59 @@ struct Lc<0> { static constexpr int m = 0, pitch = 1, size = 0, off = 0; };
 constexpr int kCoarseStack = Lc<kCoarseTop2d>::off + Lc<kCoarseTop2d>::size;
 constexpr int kCoarseWords = 2 * kCoarseStack + Lc<kCoarseTop2d>::size;   // x, b, r
 
+// level coefficients in registers
+struct Cf {
+    double c0, cx, cy, cd;
+    bool diag;
+    HW_DEV Cf(const double *c) : c0(c[kC0]), cx(c[kCx]), cy(c[kCy]), cd(c[kCd]), diag(c[kCd] != 0.0) {}
+};
+
 // one point update in CSR column order (the reference's arithmetic)
 template <int L>
-__device__ __forceinline__ void gs_point(double *x, const double *b, const double *c, int i, int j)
+__device__ __forceinline__ void gs_point(double *x, const double *b, const Cf &c, int i, int j)
 {
     constexpr int m = Lc<L>::m, p = Lc<L>::pitch;
     const int k = i * p + j;
     double acc = b[k];
-    if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[k - p - 1]);
-    if (i > 0) acc = sub_mul(acc, c[kCx], x[k - p]);
-    if (j > 0) acc = sub_mul(acc, c[kCy], x[k - 1]);
-    if (j < m - 1) acc = sub_mul(acc, c[kCy], x[k + 1]);
-    if (i < m - 1) acc = sub_mul(acc, c[kCx], x[k + p]);
-    if (i < m - 1 && j < m - 1 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[k + p + 1]);
-    x[k] = __ddiv_rn(acc, c[kC0]);
+    if (i > 0 && j > 0 && c.diag) acc = sub_mul(acc, c.cd, x[k - p - 1]);
+    if (i > 0) acc = sub_mul(acc, c.cx, x[k - p]);
+    if (j > 0) acc = sub_mul(acc, c.cy, x[k - 1]);
+    if (j < m - 1) acc = sub_mul(acc, c.cy, x[k + 1]);
+    if (i < m - 1) acc = sub_mul(acc, c.cx, x[k + p]);
+    if (i < m - 1 && j < m - 1 && c.diag) acc = sub_mul(acc, c.cd, x[k + p + 1]);
+    x[k] = __ddiv_rn(acc, c.c0);
 }
 
-// lexicographic GS (forward) or its reverse by anti-diagonal wavefronts
+// Three lexicographic GS sweeps (forward) or three of their reverse, by
+// anti-diagonal wavefronts with the sweeps PIPELINED three diagonals apart:
+// at step tau sweep s updates diagonal tau - 3s.  A point reads the new
+// values of its lower neighbours (diagonals d-1, d-2: this sweep, steps
+// tau-1, tau-2) and the previous sweep's values of its upper neighbours
+// (d+1, d+2: updated by sweep s-1 at steps tau-2, tau-1, not yet by sweep
+// s), and within one step no sweep writes a diagonal another one reads --
+// so every point sees exactly the operands of three sequential sweeps
+// (bit-identical), in 2m+5 steps instead of 3(2m-1).  m <= 31: one grid row
+// per lane.
 template <int L>
-__device__ __forceinline__ void coarse_sweep(double *xw, const double *bw, const double *c,
-                                             bool forward, int lane)
+__device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, const Cf &c,
+                                              bool forward, int lane)
 {
     constexpr int m = Lc<L>::m;
+    constexpr int D = 2 * m - 1;                       // diagonals per sweep
+    static_assert(m <= 32, "one grid row per lane");
     double *x = xw + Lc<L>::off;
     const double *b = bw + Lc<L>::off;
-    for (int dd = 0; dd <= 2 * m - 2; ++dd) {
-        const int d = forward ? dd : 2 * m - 2 - dd;
-        const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
-        const int ihi = d < m - 1 ? d : m - 1;
-        for (int i = ilo + lane; i <= ihi; i += 32) gs_point<L>(x, b, c, i, d - i);
+    for (int tau = 0; tau < D + 6; ++tau) {
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            const int dd = tau - 3 * s;
+            if (dd < 0 || dd >= D) continue;
+            const int d = forward ? dd : D - 1 - dd;
+            const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
+            const int ihi = d < m - 1 ? d : m - 1;
+            const int i = ilo + lane;
+            if (i <= ihi) gs_point<L>(x, b, c, i, d - i);
+        }
         __syncwarp();
     }
 }
@@ -465,7 +489,8 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
     if constexpr (L >= 2) {
         constexpr int m = Lc<L>::m, p = Lc<L>::pitch, mc = Lc<L - 1>::m, pc = Lc<L - 1>::pitch;
         const double *c = coef + L * kCoefStride;
-        for (int s = 0; s < 3; ++s) coarse_sweep<L>(xw, bw, c, true, lane);
+        const Cf cf(c);
+        coarse_sweep3<L>(xw, bw, cf, true, lane);
         double *x = xw + Lc<L>::off;
         const double *b = bw + Lc<L>::off;
         for (int k = lane; k < m * m; k += 32) {           // residual
@@ -520,7 +545,7 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
             x[q] = add_rn(x[q], acc);
         }
         __syncwarp();
-        for (int s = 0; s < 3; ++s) coarse_sweep<L>(xw, bw, c, false, lane);
+        coarse_sweep3<L>(xw, bw, cf, false, lane);
     } else {
         if (lane == 0) xw[0] = add_mul(0.0, coef[1 * kCoefStride + kCoarse], bw[0]);  // 1x1 solve
         __syncwarp();
