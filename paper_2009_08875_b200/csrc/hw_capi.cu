@@ -731,7 +731,10 @@ int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
         CK(launch_dot(c->p, c->q, nt, nx, c->part, c->tmp, c->scal + 1, st, &c->launches));
         CK(launch_pcg_alpha(c->scal, st));
         const bool recompute = (k % recompute_every) == 0;
-        CK(launch_update_wr(w, c->r, c->p, c->q, c->scal, N, recompute ? 0 : 1, st));
+        // r -= alpha q now; w += alpha p is deferred into the p update below
+        // (one pass over p), except before a residual recomputation, which
+        // needs the current w
+        CK(launch_update_wr(w, c->r, c->p, c->q, c->scal, N, recompute ? 1 : 0, recompute ? 0 : 1, st));
         c->launches += 2;
         CK(cudaEventRecord(ev[3], st));
         if (recompute) {
@@ -746,7 +749,7 @@ int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
         ++c->launches;
         CK(cudaMemcpyAsync(c->hscal + 1, c->scal + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(launch_pcg_beta(c->scal, st));
-        CK(launch_update_p(c->p, c->z, c->scal, N, st));
+        CK(launch_update_wp(w, c->p, c->z, c->scal, N, recompute ? 0 : 1, st));
         c->launches += 2;
         CK(cudaMemcpyAsync(c->hscal + 3, c->scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(ev[6], st));

@@ -112,9 +112,9 @@ cudaError_t launch_dot(const double *X, const double *Y, int64_t rows, int64_t n
 cudaError_t launch_pcg_alpha(double *s, cudaStream_t st);
 cudaError_t launch_pcg_beta(double *s, cudaStream_t st);
 cudaError_t launch_update_wr(double *w, double *r, const double *p, const double *q,
-                             const double *s, int64_t n, int update_r, cudaStream_t st);
-cudaError_t launch_update_p(double *p, const double *z, const double *s, int64_t n,
-                            cudaStream_t st);
+                             const double *s, int64_t n, int do_w, int do_r, cudaStream_t st);
+cudaError_t launch_update_wp(double *w, double *p, const double *z, const double *s, int64_t n,
+                             int do_w, cudaStream_t st);
 cudaError_t launch_sub(const double *f, const double *t, double *r, int64_t n, cudaStream_t st);
 cudaError_t launch_any_nonzero(const double *X, int64_t n, int *flag, cudaStream_t st);
 cudaError_t launch_row_partials(const double *X, const double *Y, int64_t rows, int64_t nx,

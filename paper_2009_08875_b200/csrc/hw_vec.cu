@@ -69,28 +69,35 @@ __global__ void pcg_beta(double *s)
     s[0] = s[2];
 }
 
-// w += alpha p ; r -= alpha q  (axpy_rows, _kernels.py:64-68; solver.py:223-235)
+// w += alpha p (if do_w) ; r -= alpha q (if do_r)  (axpy_rows, _kernels.py:64-68;
+// solver.py:223-235)
 __global__ void pcg_update_wr(double *__restrict__ w, double *__restrict__ r,
                               const double *__restrict__ p, const double *__restrict__ q,
-                              const double *__restrict__ s, int64_t n, int update_r)
+                              const double *__restrict__ s, int64_t n, int do_w, int do_r)
 {
     const double alpha = s[3];
     const double nalpha = -alpha;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
-        w[e] = add_rn(w[e], mul_rn(alpha, p[e]));
-        if (update_r) r[e] = add_rn(r[e], mul_rn(nalpha, q[e]));
+        if (do_w) w[e] = add_rn(w[e], mul_rn(alpha, p[e]));
+        if (do_r) r[e] = add_rn(r[e], mul_rn(nalpha, q[e]));
     }
 }
 
-// p = z + beta p  (xpay_rows, _kernels.py:71-76)
-__global__ void pcg_update_p(double *__restrict__ p, const double *__restrict__ z,
-                             const double *__restrict__ s, int64_t n)
+// w += alpha p (deferred from the alpha step, if do_w) and p = z + beta p
+// (xpay_rows, _kernels.py:71-76) in one pass over p: the same elementwise
+// operations as the reference's two separate updates, one read of p saved
+__global__ void pcg_update_wp(double *__restrict__ w, double *__restrict__ p,
+                              const double *__restrict__ z, const double *__restrict__ s,
+                              int64_t n, int do_w)
 {
-    const double beta = s[4];
+    const double alpha = s[3], beta = s[4];
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-         e += (int64_t)gridDim.x * blockDim.x)
-        p[e] = add_rn(z[e], mul_rn(beta, p[e]));
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const double pe = p[e];
+        if (do_w) w[e] = add_rn(w[e], mul_rn(alpha, pe));
+        p[e] = add_rn(z[e], mul_rn(beta, pe));
+    }
 }
 
 // r = f - t (periodic residual recomputation, solver.py:227-229)
@@ -182,16 +189,16 @@ cudaError_t launch_pcg_beta(double *s, cudaStream_t st)
 }
 
 cudaError_t launch_update_wr(double *w, double *r, const double *p, const double *q,
-                             const double *s, int64_t n, int update_r, cudaStream_t st)
+                             const double *s, int64_t n, int do_w, int do_r, cudaStream_t st)
 {
-    pcg_update_wr<<<grid_for(n, 256), 256, 0, st>>>(w, r, p, q, s, n, update_r);
+    pcg_update_wr<<<grid_for(n, 256), 256, 0, st>>>(w, r, p, q, s, n, do_w, do_r);
     return cudaGetLastError();
 }
 
-cudaError_t launch_update_p(double *p, const double *z, const double *s, int64_t n,
-                            cudaStream_t st)
+cudaError_t launch_update_wp(double *w, double *p, const double *z, const double *s, int64_t n,
+                             int do_w, cudaStream_t st)
 {
-    pcg_update_p<<<grid_for(n, 256), 256, 0, st>>>(p, z, s, n);
+    pcg_update_wp<<<grid_for(n, 256), 256, 0, st>>>(w, p, z, s, n, do_w);
     return cudaGetLastError();
 }
 

@@ -263,3 +263,24 @@ def test_mg_rows_fused_inner_product(K):
     assert torch.equal(X1, X2)
     scale = (Y.abs() * X1.abs()).sum(dim=1)
     assert float(((p1 - p2).abs() / scale).max()) <= 1e-14
+
+
+def test_pcg_residual_recomputation_matches_oracle():
+    """recompute_every = 4 (solver.py:227-229: r = f - S w every 4th step)
+    exercises the un-deferred w update path; iterations and u as the oracle."""
+    from oracle import heatwave_oracle as O
+
+    d, J, K, dist, u0 = inputs.recipe(1)
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** d
+    F = inputs.forcing(dist, n_t, n_x)
+    asm = hw.assemble_system(hw.ProblemData(D=np.eye(d), c=0.0, u0=u0), J, K, hw.SolveConfig(),
+                             forcing=F)
+    ref = O.assemble(d, J, K)
+    fo = ref.rhs(F, u0)
+    eps = 1e-6 * np.sqrt(O.dot(fo, ref.kx(fo)))
+    res = hw.pcg(asm.S, asm.K_X, asm.rhs, eps, recompute_every=4)
+    ro = O.pcg(ref, fo, eps, recompute_every=4)
+    assert res.iterations == ro.iterations
+    u = asm.wavelet.apply_array(res.w.array)
+    uo = ref.wavelet.apply(ro.w)
+    assert np.linalg.norm(u - uo) / np.linalg.norm(uo) <= 1e-8
