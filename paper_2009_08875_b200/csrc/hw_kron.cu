@@ -109,6 +109,11 @@ __device__ __forceinline__ bool interior_of(const Pt &p, const Grid &g)
     return p.i > 0 && p.j > 0 && p.i < g.m - 1 && p.j < g.m - 1;
 }
 
+// temporal rows per CTA of the row-streaming stencil kernels; the next
+// rows' points are prefetched into L2 two rows ahead (these kernels are
+// latency-bound on their 7-point loads otherwise)
+constexpr int kBtRows = 16;
+
 // YM = M X, YA = A X (either output may be null)
 template <bool DM, bool DA>
 __global__ void __launch_bounds__(TX * TY) stencil_rows(const double *__restrict__ X,
@@ -120,10 +125,14 @@ __global__ void __launch_bounds__(TX * TY) stencil_rows(const double *__restrict
     if (!p.ok) return;
     const int k = (int)pidx(p, g);
     const bool in = interior_of(p, g);
-    for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) {
-        const int64_t o = r * g.nx + k;
-        if (YM) YM[o] = stencil_at<DM>(X + o, p, g, in, M);
-        if (YA) YA[o] = stencil_at<DA>(X + o, p, g, in, A);
+    for (int64_t r0 = (int64_t)blockIdx.z * kBtRows; r0 < rows; r0 += (int64_t)gridDim.z * kBtRows) {
+        const int64_t r1 = r0 + kBtRows < rows ? r0 + kBtRows : rows;
+        for (int64_t r = r0; r < r1; ++r) {
+            const int64_t o = r * g.nx + k;
+            if (r + 2 < r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(X + o + 2 * g.nx));
+            if (YM) YM[o] = stencil_at<DM>(X + o, p, g, in, M);
+            if (YA) YA[o] = stencil_at<DA>(X + o, p, g, in, A);
+        }
     }
 }
 
@@ -140,11 +149,18 @@ __global__ void __launch_bounds__(TX * TY) bt_side(const double *__restrict__ G1
     if (!p.ok) return;
     const int k = (int)pidx(p, g);
     const bool in = interior_of(p, g);
-    for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) {
-        const int64_t o = r * g.nx + k;
-        double v = add_rn(stencil_at<DM>(G1 + o, p, g, in, M), stencil_at<DA>(G2 + o, p, g, in, A));
-        if (r == 0 && E0) v = add_rn(v, E0[k]);
-        out[o] = v;
+    for (int64_t r0 = (int64_t)blockIdx.z * kBtRows; r0 < rows; r0 += (int64_t)gridDim.z * kBtRows) {
+        const int64_t r1 = r0 + kBtRows < rows ? r0 + kBtRows : rows;
+        for (int64_t r = r0; r < r1; ++r) {
+            const int64_t o = r * g.nx + k;
+            if (r + 2 < r1) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(G1 + o + 2 * g.nx));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(G2 + o + 2 * g.nx));
+            }
+            double v = add_rn(stencil_at<DM>(G1 + o, p, g, in, M), stencil_at<DA>(G2 + o, p, g, in, A));
+            if (r == 0 && E0) v = add_rn(v, E0[k]);
+            out[o] = v;
+        }
     }
 }
 
@@ -158,6 +174,8 @@ __device__ __forceinline__ double band3(const double *__restrict__ tri, int64_t 
     acc = add_rn(acc, mul_rn(__ldg(b + 1), v0));
     return add_rn(acc, mul_rn(__ldg(b + 2), vp));
 }
+
+constexpr int kBsidePf = 2;
 
 // B-side, fused: t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU with
 // MxU = M_x U, AxU = A_x U computed on the fly (system.py:119-139).  Each
@@ -195,6 +213,10 @@ __global__ void __launch_bounds__(TX * TY) bside_fused(const double *__restrict_
         st(c0, m0, a0);
         if (c0 == 0 && E0) E0[k] = m0;
         for (int64_t c = c0; c < c1; ++c) {
+            // keep ~kBsidePf rows of U in flight: L2 prefetch of this thread's
+            // point kBsidePf rows ahead (the 7-point halo lines come along)
+            if (c + kBsidePf < nt && c + kBsidePf < c1 + 1)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(Uk + (c + kBsidePf - u0) * g.nx));
             double mp = 0.0, ap = 0.0;                 // row c+1
             if (c + 1 < nt) st(c + 1, mp, ap);
             const int64_t o = (c - r0) * g.nx + k;
@@ -271,7 +293,10 @@ cudaError_t launch_stencil_rows(const double *X, double *YM, double *YA, Grid g,
                                 Stencil A, int64_t rows, cudaStream_t st)
 {
     const bool dm = M.cd != 0.0, da = A.cd != 0.0;
-    const dim3 grid = spatial_grid(g, rows), block(TX, TY);
+    dim3 grid = spatial_grid(g, 1);
+    const int64_t zb = (rows + kBtRows - 1) / kBtRows;
+    grid.z = (unsigned)(zb < 65535 ? (zb < 1 ? 1 : zb) : 65535);
+    const dim3 block(TX, TY);
     if (dm && da) stencil_rows<true, true><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
     else if (dm) stencil_rows<true, false><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
     else if (da) stencil_rows<false, true><<<grid, block, 0, st>>>(X, YM, YA, g, M, A, rows);
@@ -283,7 +308,10 @@ cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0,
                            Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st)
 {
     const bool dm = M.cd != 0.0, da = A.cd != 0.0;
-    const dim3 grid = spatial_grid(g, rows), block(TX, TY);
+    dim3 grid = spatial_grid(g, 1);
+    const int64_t zb = (rows + kBtRows - 1) / kBtRows;
+    grid.z = (unsigned)(zb < 65535 ? (zb < 1 ? 1 : zb) : 65535);
+    const dim3 block(TX, TY);
     if (dm && da) bt_side<true, true><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
     else if (dm) bt_side<true, false><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
     else if (da) bt_side<false, true><<<grid, block, 0, st>>>(G1, G2, E0, out, g, M, A, rows);
