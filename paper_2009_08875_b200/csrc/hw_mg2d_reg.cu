@@ -35,6 +35,8 @@
 #include "hw_common.cuh"
 #include "hw_internal.cuh"
 
+#include <cstdint>
+
 namespace hw {
 namespace {
 
@@ -48,6 +50,10 @@ HW_DEV void cp_async8z(void *smem, const void *gmem, bool valid)
 HW_DEV void cp_async8s(unsigned saddr, const void *gmem)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
+}
+HW_DEV void cp_async16s(unsigned saddr, const void *gmem)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
 HW_DEV unsigned smem_u32(const void *p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -173,7 +179,7 @@ struct RegPass {
         tot = HRes + HS;
         for (int k = tid; k < SM::total; k += NT) sm[k] = 0.0;   // pads stay zero
         cpo = phys(tid);
-        hoff = phys(P * (tid + 1));
+        hoff = phys(P * (tid + 1)) ^ (DOWN ? 0 : 1);          // UP rows are pair-swapped
 #pragma unroll
         for (int h = 0; h < P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
         sb = 4;                                // step -3 (the prologue's first group)
@@ -208,6 +214,11 @@ struct RegPass {
     // pad columns n, n+1 are never written and stay zero).  Rows >= n: ZERO
     // writes a zero row (x0 row n is the grid's zero boundary row), else the
     // copy is skipped (such b / x0 rows only feed discarded sweeps).
+    // Rows whose column pairs (2p, 2p+1) are 16-byte units in global memory
+    // (half of them: n is odd) are copied 16 bytes at a time.  UP reads its
+    // rows point-reversed, so a 16-byte unit lands pair-swapped; UP therefore
+    // keeps EVERY staged row pair-swapped (8-byte copies too) and its
+    // consumers swap back at compile time (load_chunk, hoff).
     template <bool ZERO>
     HW_DEV void stage_row(double *slot, const double *src, int i) const
     {
@@ -218,11 +229,25 @@ struct RegPass {
             }
             return;
         }
-        const double *g = src + gidx(i, 0) + gs * tid;
-        const unsigned sa = smem_u32(slot + cpo);
+        const double *row0 = src + gidx(i, 0);               // local column 0
+        const double *a16 = DOWN ? row0 : row0 - 1;          // start of unit (0, 1)
+        if ((reinterpret_cast<uintptr_t>(a16) & 15) == 0) {
+            const unsigned sa = smem_u32(slot + phys(2 * tid));
 #pragma unroll
-        for (int k = 0; k < P; ++k)
-            if (k < P - 1 || tid < NT - 1) cp_async8s(sa + 8u * koff(k), g + gs * k * NT);
+            for (int k = 0; k < P / 2; ++k) {
+                const int q = tid + k * NT;                  // pair (2q, 2q+1)
+                if (k < P / 2 - 1 || tid < NT - 1)
+                    cp_async16s(sa + 16u * k * NT, DOWN ? row0 + 2 * q : row0 - 2 * q - 1);
+                else                                         // column n-1 only (n is a pad)
+                    cp_async8s(sa + 16u * k * NT + (DOWN ? 0u : 8u), row0 + gs * (2 * q));
+            }
+        } else {
+            const double *g = row0 + gs * tid;
+            const unsigned sa = smem_u32(slot + (DOWN ? cpo : (cpo ^ 1)));
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+                if (k < P - 1 || tid < NT - 1) cp_async8s(sa + 8u * koff(k), g + gs * k * NT);
+        }
     }
     // coarse row ic, local columns 0..m-1 at slot index J+1 (index 0 and m+1
     // stay zero); rows -1 and m are zero rows
@@ -262,8 +287,8 @@ struct RegPass {
 #pragma unroll
         for (int h = 0; h < P / 2; ++h) {
             const double2 w = *reinterpret_cast<const double2 *>(slot + ooff[h]);
-            v[2 * h] = w.x;
-            v[2 * h + 1] = w.y;
+            v[2 * h] = DOWN ? w.x : w.y;                     // UP rows are pair-swapped
+            v[2 * h + 1] = DOWN ? w.y : w.x;
         }
     }
 
