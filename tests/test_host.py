@@ -152,3 +152,18 @@ def test_library_has_no_undefined_internal_symbols():
     out = subprocess.run(["nm", "-D", "--undefined-only", so], capture_output=True, text=True).stdout
     missing = [ln.split()[-1] for ln in out.splitlines() if "_ZN2hw" in ln]
     assert not missing, missing
+
+
+def test_bench_implementation_byte_model():
+    """Per-iteration algorithmic bytes of this implementation (bench.py
+    roofline_iteration): 2D K = 10 streams ~90 words per DoF, dominated by
+    the three batched multigrid applications; 1D streams 35."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    N4 = (2 ** 10 + 1) * (2 ** 10 - 1) ** 2
+    w4 = bench.impl_bytes_per_iteration(2, 10, 10) / 8 / N4
+    assert 85 < w4 < 95, w4
+    N3 = (2 ** 20 + 1) * (2 ** 10 - 1)
+    assert abs(bench.impl_bytes_per_iteration(1, 20, 10) / 8 / N3 - 35.0) < 0.01
