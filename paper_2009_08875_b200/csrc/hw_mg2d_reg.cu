@@ -78,7 +78,9 @@ struct RegSmem {
     static constexpr int total = B + X0 + C + O + H;
 };
 
-template <int P, int NT, bool DOWN, bool ZS>
+// LB0 / LX0 (UP only): layout parity of grid row 0 of b / x0 (stage_row);
+// row i has parity L0 ^ (i & 1) because a grid row is n (odd) words long
+template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0>
 struct RegPass {
     static constexpr int NW = NT / 32;
     static constexpr int n = P * NT - 1;
@@ -107,8 +109,8 @@ struct RegPass {
     double *bsm, *x0sm, *csm, *osm;
     double *HR, *HRes, *tot;              // [3][HS], [1][HS], [3][HS]
     int cpo;                              // slot position of column tid (copy / flush lane)
-    int hoff;                             // slot position of the right-halo column P (t+1)
-    int ooff[P / 2];                      // slot positions of the own chunk's 16-byte pairs
+    int hoff;                             // DOWN: slot position of the right-halo column P (t+1)
+    int ooff[P / 2 + 1];                  // slot positions of units P t/2 .. P t/2 + P/2
     int sb, sx;                           // ring slots of b(t) and x0(t+1) at step t
     int sc;                               // UP: ring slot of coarse row floor(t/2) at step t
     double HC[NC];                        // UP: 0.5 x the latest coarse row this thread reads
@@ -179,9 +181,9 @@ struct RegPass {
         tot = HRes + HS;
         for (int k = tid; k < SM::total; k += NT) sm[k] = 0.0;   // pads stay zero
         cpo = phys(tid);
-        hoff = phys(P * (tid + 1)) ^ (DOWN ? 0 : 1);          // UP rows are pair-swapped
+        hoff = phys(P * (tid + 1));
 #pragma unroll
-        for (int h = 0; h < P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
+        for (int h = 0; h <= P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
         sb = 4;                                // step -3 (the prologue's first group)
         sx = 1;
         sc = 0;                                // coarse row 0 at steps 0, 1
@@ -210,43 +212,68 @@ struct RegPass {
 
     HW_DEV int koff(int k) const { return LIN ? k * NT : phys(tid + k * NT) - cpo; }
 
-    // cooperative coalesced stage of fine row i of src (columns 0..n-1; the
-    // pad columns n, n+1 are never written and stay zero).  Rows >= n: ZERO
+    // Cooperative coalesced stage of fine row i of src (columns 0..n-1; the
+    // pad columns -1, n, n+1 are never written by a copy).  Rows >= n: ZERO
     // writes a zero row (x0 row n is the grid's zero boundary row), else the
     // copy is skipped (such b / x0 rows only feed discarded sweeps).
-    // Rows whose column pairs (2p, 2p+1) are 16-byte units in global memory
-    // (half of them: n is odd) are copied 16 bytes at a time.  UP reads its
-    // rows point-reversed, so a 16-byte unit lands pair-swapped; UP therefore
-    // keeps EVERY staged row pair-swapped (8-byte copies too) and its
-    // consumers swap back at compile time (load_chunk, hoff).
-    template <bool ZERO>
+    //  DOWN: natural layout; rows whose column pairs (2p, 2p+1) are 16-byte
+    //   units in global memory (half of them, n is odd) are copied 16 bytes
+    //   at a time, the others 8 bytes.
+    //  UP (LR = layout parity): the slot holds the row's global 16-byte
+    //   units, columns (2u - LR, 2u + 1 - LR), in address order (so each
+    //   unit's columns are swapped: UP reads point-reversed); every copy is
+    //   16 bytes but the half-units at the row ends.  UP is bound by its
+    //   copy-instruction count; DOWN is not (the parity variants cost it
+    //   more than they saved).
+    template <bool ZERO, int LR>
     HW_DEV void stage_row(double *slot, const double *src, int i) const
     {
         if (i >= n) {
             if constexpr (ZERO) {
 #pragma unroll
-                for (int k = 0; k < P; ++k) slot[cpo + koff(k)] = 0.0;
+                for (int k = 0; k < P; ++k) slot[tid + k * NT] = 0.0;
             }
             return;
         }
         const double *row0 = src + gidx(i, 0);               // local column 0
-        const double *a16 = DOWN ? row0 : row0 - 1;          // start of unit (0, 1)
-        if ((reinterpret_cast<uintptr_t>(a16) & 15) == 0) {
+        if constexpr (DOWN) {
+            if ((reinterpret_cast<uintptr_t>(row0) & 15) == 0) {
+                const unsigned sa = smem_u32(slot + phys(2 * tid));
+#pragma unroll
+                for (int k = 0; k < P / 2; ++k) {
+                    const int q = tid + k * NT;              // pair (2q, 2q+1)
+                    if (k < P / 2 - 1 || tid < NT - 1)
+                        cp_async16s(sa + 16u * k * NT, row0 + 2 * q);
+                    else                                     // column n-1 only (n is a pad)
+                        cp_async8s(sa + 16u * k * NT, row0 + 2 * q);
+                }
+            } else {
+                const double *g = row0 + tid;
+                const unsigned sa = smem_u32(slot + cpo);
+#pragma unroll
+                for (int k = 0; k < P; ++k)
+                    if (k < P - 1 || tid < NT - 1) cp_async8s(sa + 8u * koff(k), g + k * NT);
+            }
+        } else {
             const unsigned sa = smem_u32(slot + phys(2 * tid));
 #pragma unroll
             for (int k = 0; k < P / 2; ++k) {
-                const int q = tid + k * NT;                  // pair (2q, 2q+1)
-                if (k < P / 2 - 1 || tid < NT - 1)
-                    cp_async16s(sa + 16u * k * NT, DOWN ? row0 + 2 * q : row0 - 2 * q - 1);
-                else                                         // column n-1 only (n is a pad)
-                    cp_async8s(sa + 16u * k * NT + (DOWN ? 0u : 8u), row0 + gs * (2 * q));
+                const int q = tid + k * NT;                  // unit q
+                const unsigned d = sa + 16u * k * NT;
+                if constexpr (LR == 0) {                     // columns (2q, 2q+1)
+                    if (k < P / 2 - 1 || tid < NT - 1) {
+                        cp_async16s(d, row0 - 2 * q - 1);
+                    } else {                                 // (n-1, n): column n-1 only;
+                        cp_async8s(d + 8u, row0 - 2 * q);
+                        // the pad n: the slot may last have held a parity-1
+                        // row, whose unit here was full
+                        slot[phys(2 * q)] = 0.0;
+                    }
+                } else {                                     // columns (2q-1, 2q)
+                    if (k > 0 || tid > 0) cp_async16s(d, row0 - 2 * q);
+                    else cp_async8s(d, row0);                // (-1, 0): column 0 only
+                }
             }
-        } else {
-            const double *g = row0 + gs * tid;
-            const unsigned sa = smem_u32(slot + (DOWN ? cpo : (cpo ^ 1)));
-#pragma unroll
-            for (int k = 0; k < P; ++k)
-                if (k < P - 1 || tid < NT - 1) cp_async8s(sa + 8u * koff(k), g + gs * k * NT);
         }
     }
     // coarse row ic, local columns 0..m-1 at slot index J+1 (index 0 and m+1
@@ -274,32 +301,42 @@ struct RegPass {
     template <int TPAR>                // TPAR = t & 1
     HW_DEV void issue(int t) const
     {
-        stage_row<false>(bsm + (size_t)bslot(4) * RS, Bg, t + 3);
-        if constexpr (!(DOWN && ZS)) stage_row<true>(x0sm + (size_t)sx * RS, Xg, t + 4);
+        stage_row<false, LB0 ^ TPAR ^ 1>(bsm + (size_t)bslot(4) * RS, Bg, t + 3);
+        if constexpr (!(DOWN && ZS)) stage_row<true, LX0 ^ TPAR>(x0sm + (size_t)sx * RS, Xg, t + 4);
         if constexpr (!DOWN && TPAR == 0)    // coarse row floor(t/2) + 2 (even t)
             stage_coarse((t + 4) / 2, sc + 2 >= SM::NCR ? sc + 2 - SM::NCR : sc + 2);
         cp_async_commit();
     }
 
-    // own chunk (P values) of a staged row
-    HW_DEV void load_chunk(const double *slot, double v[P]) const
+    // own chunk (v[0..P-1]) of a staged row; UP rows of layout parity 1 also
+    // yield the right-halo column v[P] from the extra unit
+    template <int LR>
+    HW_DEV void load_chunk(const double *slot, double v[P + 1]) const
     {
+        constexpr int L = DOWN ? 0 : LR;
 #pragma unroll
-        for (int h = 0; h < P / 2; ++h) {
+        for (int h = 0; h < P / 2 + L; ++h) {
             const double2 w = *reinterpret_cast<const double2 *>(slot + ooff[h]);
-            v[2 * h] = DOWN ? w.x : w.y;                     // UP rows are pair-swapped
-            v[2 * h + 1] = DOWN ? w.y : w.x;
+            const double lo = DOWN ? w.x : w.y, hi = DOWN ? w.y : w.x;   // lower / upper column
+            if constexpr (L == 0) {
+                v[2 * h] = lo;
+                v[2 * h + 1] = hi;
+            } else {
+                if (h > 0) v[2 * h - 1] = lo;
+                v[2 * h] = hi;
+            }
         }
     }
 
     // x0 row i (P+1 values) from its slot; UP adds the prolongated coarse
     // correction (same arithmetic as mg2d_stream's prolongate)
-    template <int IPAR, bool EDGE>
+    template <int IPAR, bool EDGE, int LR>
     HW_DEV void load_x0(int i, int slotno, int cslot, double v[P + 1])
     {
         const double *slot = x0sm + (size_t)slotno * RS;
-        load_chunk(slot, v);
-        v[P] = slot[hoff];
+        load_chunk<LR>(slot, v);
+        if constexpr (DOWN) v[P] = slot[hoff];                         // right halo
+        else if constexpr (LR == 0) v[P] = slot[ooff[P / 2] + 1];
         if constexpr (!DOWN) {
             if (EDGE && i >= n) return;                  // row n stays a zero pad
             // coarse rows c_a = floor((i-1)/2) and, for even i, c_a + 1.  Row
@@ -337,9 +374,10 @@ struct RegPass {
         }
     }
 
-    HW_DEV void load_b(int back, double b[P]) const
+    template <int LR>
+    HW_DEV void load_b(int back, double b[P + 1]) const
     {
-        load_chunk(bsm + (size_t)bslot(back) * RS, b);
+        load_chunk<LR>(bsm + (size_t)bslot(back) * RS, b);
     }
 
     // coalesced copy of the staged output row (grid row i) to global memory
@@ -424,22 +462,23 @@ struct RegPass {
         }
 
         // ---- phase A: chunk recurrences of the three sweeps ----
-        double y[3][P], b[P];
+        double y[3][P], b[P + 1];
+        constexpr int LBr = LB0 ^ PAR, LXr = LX0 ^ PAR ^ 1;   // UP parities of b(t), x0(t+1)
         double dn0[P + 1];
         if constexpr (DOWN && ZS) {
             double z[P];
 #pragma unroll
             for (int k = 0; k < P; ++k) z[k] = 0.0;
-            load_b(0, b);
+            load_b<LBr>(0, b);
             chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0]);
         } else {
-            load_x0<Q, EDGE>(t + 1, sx, sc, dn0);
-            load_b(0, b);
+            load_x0<Q, EDGE, LXr>(t + 1, sx, sc, dn0);
+            load_b<LBr>(0, b);
             chunk(X1[Q], X1L, X0n, X0n[P], dn0, dn0[P], b, y[0]);
         }
-        load_b(2, b);
+        load_b<LBr>(2, b);
         chunk(X2[Q], X2L, X1[PAR], X1R[PAR], X1[Q], X1R[Q], b, y[1]);
-        load_b(4, b);
+        load_b<LBr>(4, b);
         chunk(X3, X3L, X2[PAR], X2R[PAR], X2[Q], X2R[Q], b, y[2]);
 
         // residual of grid row t-6 from d(t-6), d(t-5)
@@ -552,7 +591,7 @@ struct RegPass {
         // -3..-1 would have issued
         __syncthreads();                                 // zeroed slots before any copy lands
         if constexpr (!(DOWN && ZS)) {
-            stage_row<true>(x0sm, Xg, 0);
+            stage_row<true, LX0>(x0sm, Xg, 0);
             if constexpr (!DOWN) {
                 stage_coarse(-1, SM::NCR - 1);
                 stage_coarse(0, 0);
@@ -567,7 +606,7 @@ struct RegPass {
         if constexpr (!(DOWN && ZS)) {
             cp_async_wait<2>();
             __syncthreads();
-            load_x0<0, true>(0, 0, SM::NCR - 1, X0n);
+            load_x0<0, true, LX0>(0, 0, SM::NCR - 1, X0n);
             __syncthreads();                             // x0(3) reuses x0(0)'s slot
         }
         issue<1>(-1);
@@ -591,13 +630,38 @@ struct RegPass {
     }
 };
 
+template <int P, int NT, bool DOWN, bool ZS, int LB, int LX>
+HW_DEV void run_pass(const MgStreamArgs &a, double *sm)
+{
+    RegPass<P, NT, DOWN, ZS, LB, LX> p(a, sm);
+    p.run();
+    p.finish_dot(a);
+}
+
 template <int P, int NT, bool DOWN, bool ZS, int MINB>
 __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
 {
     extern __shared__ __align__(16) double sm[];
-    RegPass<P, NT, DOWN, ZS> p(a, sm);
-    p.run();
-    p.finish_dot(a);
+    if constexpr (DOWN) {
+        run_pass<P, NT, DOWN, ZS, 0, 0>(a, sm);
+    } else {
+        // UP: layout parity of grid row 0 (stage_row) = 1 when local column 0
+        // (global row n-1, column n-1) sits at a 16-byte boundary
+        constexpr int n = P * NT - 1;
+        const int64_t row = blockIdx.x;
+        auto parity = [&](const double *base, int64_t ld) -> int {
+            const double *p0 = base + row * ld + (int64_t)(n - 1) * n + (n - 1);
+            return 1 - (int)((reinterpret_cast<uintptr_t>(p0) >> 3) & 1);
+        };
+        const int lb = parity(a.B, a.ldB), lx = parity(a.X, a.ldX);
+        if (lb) {
+            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 1, 0>(a, sm);
+        } else {
+            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 0, 0>(a, sm);
+        }
+    }
 }
 
 template <int P, int NT, bool DOWN, bool ZS, int MINB>
