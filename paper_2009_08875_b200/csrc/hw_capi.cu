@@ -282,7 +282,7 @@ static int64_t level_size(const hwg_ctx *c, int l)
 // last finest-level UP pass when that pass runs on mg2d_reg, else by row_dots
 static bool mg_dot_fusable(const hwg_ctx *c)
 {
-    return c->dim == 2 && c->K >= 7 && c->K <= 10 && c->mg_reg_ok;
+    return c->dim == 2 && c->K >= 6 && c->K <= 10 && c->mg_reg_ok;
 }
 
 static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op,

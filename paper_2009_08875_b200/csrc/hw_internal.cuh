@@ -40,7 +40,7 @@ struct MgCoarseArgs {
 
 constexpr int kCoarseTop2d = 5;
 cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
-// register-resident variant (hw_mg2d_reg.cu), levels 7..10; cudaErrorNotSupported otherwise
+// register-resident variant (hw_mg2d_reg.cu), levels 6..10; cudaErrorNotSupported otherwise
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
 // largest |beta| = |cy / c0| mg2d_reg accepts (8-chunk window: |beta|^32 <= 2^-60)
 constexpr double kRegBetaMax = 0.2726;

@@ -1,5 +1,5 @@
 // hw_mg2d_reg.cu -- register-resident streamed multigrid level passes, 2D,
-// levels l = 7..10 (n = 2^l - 1 = P NT - 1 points per direction).
+// levels l = 6..10 (n = 2^l - 1 = P NT - 1 points per direction).
 //
 // Same operator as mg2d_stream (hw_mg2d.cu; the reference's _mg_core,
 // /root/reference/pkg/src/heatwave/_kernels.py:110-199): per temporal row,
@@ -87,12 +87,13 @@ struct RegPass {
     static constexpr int m = (n - 1) / 2;
     static constexpr int WIN = 32 / P;                 // chunk ends in the carry window
     static constexpr int LEV = ilog2c(WIN);            // shuffle-scan levels
-    static constexpr int NC = P / 2 + 2;               // coarse columns a thread reads
+    static constexpr int NC = (P / 2 + 3) & ~1;        // coarse columns a thread reads (even)
     static constexpr int HS = NW + 1;
     static constexpr int SWZ = P / 2 - 1;
     using SM = RegSmem<P, NT, DOWN, ZS>;
     static constexpr int RS = SM::RS, CS = SM::CS;
-    static_assert(P % 2 == 0 && 32 % P == 0 && P >= 4 && NC % 2 == 0 && CS >= m + 2, "chunk layout");
+    static_assert(P % 2 == 0 && 32 % P == 0 && P >= 2 && CS >= (P / 2) * (NT - 1) + NC &&
+                      CS >= m + 2, "chunk layout");
     static constexpr int gs = DOWN ? 1 : -1;           // UP runs point-reversed
 
     // ---- per-CTA / per-thread constants ----
@@ -347,11 +348,16 @@ struct RegPass {
             double hb[NC];
             if constexpr (!IPAR) {
                 const double *pb = csm + (size_t)(cslot + 1 == SM::NCR ? 0 : cslot + 1) * CS;
+                if constexpr ((P / 2) % 2 == 0) {            // 16-byte aligned pairs
 #pragma unroll
-                for (int q = 0; q < NC; q += 2) {
-                    const double2 w = *reinterpret_cast<const double2 *>(pb + cphys((P / 2) * tid + q));
-                    hb[q] = 0.5 * w.x;
-                    hb[q + 1] = 0.5 * w.y;
+                    for (int q = 0; q < NC; q += 2) {
+                        const double2 w = *reinterpret_cast<const double2 *>(pb + cphys((P / 2) * tid + q));
+                        hb[q] = 0.5 * w.x;
+                        hb[q + 1] = 0.5 * w.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NC; ++q) hb[q] = 0.5 * pb[cphys((P / 2) * tid + q)];
                 }
             }
 #pragma unroll
@@ -688,6 +694,7 @@ cudaError_t launch_reg_n(const MgStreamArgs &a, bool down, int64_t rows, cudaStr
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
     switch (a.n) {
+    case 63: return launch_reg_n<2, 32, 1>(a, down, rows, st);
     case 127: return launch_reg_n<4, 32, 1>(a, down, rows, st);
     case 255: return launch_reg_n<8, 32, 1>(a, down, rows, st);
     case 511: return launch_reg_n<8, 64, 1>(a, down, rows, st);
