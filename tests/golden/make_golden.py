@@ -39,15 +39,15 @@ from paper_2009_08875_b200 import inputs  # noqa: E402
 PROBE_SEED = 7
 
 
-def problem_for(d, dist):
+def problem_for(d, dist, D=None, c=0.0):
     u0 = inputs.u0_sines if dist == "uniform" else inputs.u0_modes()
-    return hw.ProblemData(D=np.eye(d), c=0.0, u0=u0)
+    return hw.ProblemData(D=np.eye(d) if D is None else np.asarray(D, dtype=float), c=c, u0=u0)
 
 
-def stencil_table(asm):
+def stencil_table(asm, problem):
     """Per-level (A, M) stencil values read from the reference's CSR."""
     out = []
-    for ops in hw.assemble_level_operators(asm.hierarchy):
+    for ops in hw.assemble_level_operators(asm.hierarchy, problem.D, problem.c):
         A = ops.A_x.to_scipy().tocsr()
         M = ops.M_x.to_scipy().tocsr()
         n = A.shape[0]
@@ -80,9 +80,9 @@ def forcing_part(asm, F):
 LEAN_DROP = ("load", "ky", "g_ss", "g_hat", "u0_hat", "MxP", "AxP", "WP")
 
 
-def run_case(name, d, J, K, dist, full=True, workers=8, lean=False):
+def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.0):
     t0 = time.time()
-    problem = problem_for(d, dist)
+    problem = problem_for(d, dist, D, c)
     asm = hw.assemble_system(problem, J, K, hw.SolveConfig())
     n_t, n_x = asm.S.n_t, asm.S.n_x
     F = inputs.forcing(dist, n_t, n_x)
@@ -99,6 +99,7 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False):
     res = hw.pcg(asm.S, asm.K_X, hw.SpaceTimeVector(fhat), eps, plan)
     u = asm.wavelet.apply_array(res.w.array)
     meta = dict(name=name, d=d, J=J, K=K, dist=dist, n_t=n_t, n_x=n_x,
+                D=np.asarray(problem.D, dtype=float).tolist(), c=float(problem.c),
                 seed_f=inputs.SEED_F, probe_seed=PROBE_SEED,
                 iterations=res.iterations, eps=eps, rho0=rho0,
                 kappa=res.kappa_estimate,
@@ -108,7 +109,7 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False):
                 F_sum=float(F.sum()), fhat_norm=float(np.linalg.norm(fhat)),
                 u_norm=float(np.linalg.norm(u)),
                 w_norm=float(np.linalg.norm(res.w.array)),
-                stencils=stencil_table(asm))
+                stencils=stencil_table(asm, problem))
     arrays = dict(u0proj=u0proj)
     rng = np.random.default_rng(PROBE_SEED)
     idx = np.sort(rng.choice(n_t * n_x, size=min(4096, n_t * n_x), replace=False))
@@ -234,6 +235,9 @@ CASES = {
     "c1": lambda: run_case("c1", 2, 4, 4, "uniform"),
     "d1": lambda: run_case("d1", 1, 6, 6, "normal"),
     "c2s": lambda: run_case("c2s", 2, 3, 6, "uniform", lean=True),
+    # anisotropic diffusion + reaction: |beta| = 0.43 along y > kRegBetaMax,
+    # so the GPU multigrid takes the shared-ring (exact-scan) fallback
+    "a1": lambda: run_case("a1", 2, 3, 6, "uniform", lean=True, D=[[1.0, 0.0], [0.0, 6.0]], c=0.5),
     "d2": lambda: run_case("d2", 1, 10, 10, "normal", full=False),
     "cfg2": lambda: run_case("cfg2", 2, 8, 8, "uniform", full=False),
     "mg8": lambda: mg_rows_case("mg8", 2, 8),

@@ -24,12 +24,13 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2009_08875_b200 as hw  # noqa: E402
 from paper_2009_08875_b200 import inputs  # noqa: E402
 
-FULL_CASES = ("c1", "d1", "c2s")
+FULL_CASES = ("c1", "d1", "c2s", "a1")
 
 
 def _problem(meta):
     u0 = inputs.u0_sines if meta["dist"] == "uniform" else inputs.u0_modes()
-    return hw.ProblemData(D=np.eye(meta["d"]), c=0.0, u0=u0)
+    D = np.asarray(meta["D"]) if "D" in meta else np.eye(meta["d"])
+    return hw.ProblemData(D=D, c=meta.get("c", 0.0), u0=u0)
 
 
 @pytest.fixture(scope="module", params=FULL_CASES)

@@ -40,12 +40,13 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("name", ["c1", "c2s", "d1"])
+@pytest.mark.parametrize("name", ["c1", "c2s", "d1", "a1"])
 def test_stencils_bit_identical_to_reference(name):
     meta, _ = golden(name)
     d = meta["d"]
+    D, c = meta.get("D"), meta.get("c", 0.0)
     for lvl, st in enumerate(meta["stencils"], start=1):
-        M, A = disc.level_stencils(d, lvl)
+        M, A = disc.level_stencils(d, lvl, D, c)
         m = 2 ** lvl - 1
         keymap = {0: "c0", 1: "cy"} if d == 1 else {0: "c0", 1: "cy", m: "cx", m + 1: "cd"}
         for ours, offs, vals in ((A, st["A_off"], st["A"]), (M, st["M_off"], st["M"])):
