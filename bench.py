@@ -370,6 +370,7 @@ def run_ours(args):
             "roofline_iteration": {"bytes_per_iteration": impl_b, "s_per_iteration": it_s,
                                    "achieved_GBs": impl_b / it_s / 1e9, "peak": peak,
                                    "frac": impl_b / it_s / 1e9 / peak,
+                                   "frac_vs_nominal_8TBs": impl_b / it_s / 8e12,
                                    "source": "algorithmic bytes of this implementation's "
                                              "kernels per PCG iteration (bench.impl_bytes_per_iteration)"},
             "roofline_model": {"bytes_per_iteration": model, "s_per_iteration": it_s,
@@ -488,6 +489,7 @@ def run_slab(args):
             "roofline_iteration": {"bytes_per_iteration": impl_b, "s_per_iteration": it_s,
                                    "achieved_GBs": impl_b / it_s / 1e9, "peak": peak * world,
                                    "frac": impl_b / it_s / 1e9 / (peak * world),
+                                   "frac_vs_nominal_8TBs": impl_b / it_s / (8e12 * world),
                                    "source": "algorithmic bytes per PCG iteration, aggregate "
                                              "over GPUs"},
             "roofline_model": {"bytes_per_iteration": model, "s_per_iteration": it_s,
