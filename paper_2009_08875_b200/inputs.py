@@ -25,6 +25,9 @@ CONFIGS = {
     2: dict(d=2, J=8, K=8, dist="uniform"),
     3: dict(d=1, J=20, K=10, dist="normal"),
     4: dict(d=2, J=10, K=10, dist="uniform"),
+    # L-shaped [-1,1]^2 \ [0,1]^2, h = 2^-10, mapped to [0,1]^2 minus
+    # [1/2,1]^2 (K = 11 there) with D = I/4 (see discretization.lshape_problem)
+    5: dict(d=2, J=11, K=11, dist="lshape", domain="L"),
 }
 
 SEED_F = 0
@@ -37,6 +40,8 @@ def _block(dist, seed, b, rows, n_x):
         return rng.uniform(-1.0, 1.0, (rows, n_x))
     if dist == "normal":
         return rng.standard_normal((rows, n_x))
+    if dist == "lshape":                      # BASELINE cfg 5: 1 + U[-0.1, 0.1]
+        return 1.0 + rng.uniform(-0.1, 0.1, (rows, n_x))
     raise ValueError(f"unknown distribution {dist!r}")
 
 
@@ -76,8 +81,21 @@ def u0_modes(seed: int = SEED_U0, modes: int = 8):
     return u0
 
 
+def u0_zero(pts):
+    """u0 = 0 (BASELINE cfg 5)."""
+    return np.zeros(len(pts))
+
+
+def u0_for(dist: str):
+    return {"uniform": u0_sines, "normal": None, "lshape": u0_zero}[dist] or u0_modes()
+
+
 def recipe(cfg: int):
     """(d, J, K, dist, u0 callable) of a BASELINE config."""
     c = CONFIGS[cfg]
-    u0 = u0_sines if c["dist"] == "uniform" else u0_modes()
-    return c["d"], c["J"], c["K"], c["dist"], u0
+    return c["d"], c["J"], c["K"], c["dist"], u0_for(c["dist"])
+
+
+def u0_by_name(name: str):
+    """The u0 callable a fixture records by name ("sines", "modes", "zero")."""
+    return {"sines": u0_sines, "zero": u0_zero}.get(name) or u0_modes()

@@ -39,9 +39,59 @@ from paper_2009_08875_b200 import inputs  # noqa: E402
 PROBE_SEED = 7
 
 
-def problem_for(d, dist, D=None, c=0.0):
-    u0 = inputs.u0_sines if dist == "uniform" else inputs.u0_modes()
+def problem_for(d, dist, D=None, c=0.0, u0=None):
+    if u0 is None:
+        u0 = inputs.u0_for(dist)
     return hw.ProblemData(D=np.eye(d) if D is None else np.asarray(D, dtype=float), c=c, u0=u0)
+
+
+def lshape_hierarchy(K):
+    """Reference ``Mesh`` / ``MeshHierarchy`` objects of the mapped L-shaped
+    domain [0,1]^2 minus [1/2,1]^2, levels 2..K.
+
+    The reference builds only the cube (spatial.py:98-137); this is its
+    square mesh (same vertex list, same element order) with the cells of the
+    removed quadrant dropped and the closed quadrant's vertices on the
+    boundary.  Everything downstream -- assemble_spatial, _build_prolongation,
+    make_solver (dense inverse of the 5-dof level 2), the Schur operator,
+    K_X, assemble_rhs, pcg -- is the reference's own code."""
+    from heatwave.spatial import Mesh, MeshHierarchy, _build_prolongation
+    levels = []
+    for k in range(2, K + 1):
+        m = 2 ** k
+        g = np.arange(m + 1)
+        X, Y = np.meshgrid(g, g, indexing="ij")
+        verts = np.stack([X.ravel(), Y.ravel()], axis=1).astype(float) / m
+        i, j = (a.ravel() for a in np.meshgrid(g[:-1], g[:-1], indexing="ij"))
+        keep = ~((i >= m // 2) & (j >= m // 2))
+        i, j = i[keep], j[keep]
+        vid = lambda a, b: a * (m + 1) + b  # noqa: E731
+        t1 = np.stack([vid(i, j), vid(i + 1, j), vid(i + 1, j + 1)], axis=1)
+        t2 = np.stack([vid(i, j), vid(i + 1, j + 1), vid(i, j + 1)], axis=1)
+        grid = np.rint(verts * m).astype(int)
+        inner = np.all((grid > 0) & (grid < m), axis=1) & ~np.all(grid >= m // 2, axis=1)
+        interior = np.where(inner)[0]
+        index = np.full(len(verts), -1, dtype=np.int64)
+        index[interior] = np.arange(len(interior))
+        levels.append(Mesh(d=2, level=k, vertices=verts, elements=np.concatenate([t1, t2]),
+                           interior=interior, interior_index=index))
+    prols = [_build_prolongation(levels[q - 1], levels[q]) for q in range(1, len(levels))]
+    return MeshHierarchy(d=2, K=len(levels), levels=levels, prolongations=prols)
+
+
+def assemble_reference(problem, J, K, domain="square"):
+    """hw.assemble_system; for the L-shaped domain the reference's own
+    assemble_system runs with build_mesh_hierarchy swapped for
+    lshape_hierarchy (its only mesh-dependent call, solver.py:360)."""
+    if domain == "square":
+        return hw.assemble_system(problem, J, K, hw.SolveConfig())
+    import heatwave.solver as hws
+    orig = hws.build_mesh_hierarchy
+    hws.build_mesh_hierarchy = lambda d, k: lshape_hierarchy(k)
+    try:
+        return hw.assemble_system(problem, J, K, hw.SolveConfig())
+    finally:
+        hws.build_mesh_hierarchy = orig
 
 
 def stencil_table(asm, problem):
@@ -77,13 +127,18 @@ def forcing_part(asm, F):
     return y, ky, g_ss, asm.wavelet.transpose_apply_array(g_ss)
 
 
+def u0_name(u0):
+    return {inputs.u0_sines: "sines", inputs.u0_zero: "zero"}.get(u0, "modes")
+
+
 LEAN_DROP = ("load", "ky", "g_ss", "g_hat", "u0_hat", "MxP", "AxP", "WP")
 
 
-def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.0):
+def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.0,
+             domain="square", u0=None):
     t0 = time.time()
-    problem = problem_for(d, dist, D, c)
-    asm = hw.assemble_system(problem, J, K, hw.SolveConfig())
+    problem = problem_for(d, dist, D, c, u0)
+    asm = assemble_reference(problem, J, K, domain)
     n_t, n_x = asm.S.n_t, asm.S.n_x
     F = inputs.forcing(dist, n_t, n_x)
     y, ky, g_ss, g_hat = forcing_part(asm, F)
@@ -98,7 +153,8 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.
     eps = 1e-6 * np.sqrt(rho0)
     res = hw.pcg(asm.S, asm.K_X, hw.SpaceTimeVector(fhat), eps, plan)
     u = asm.wavelet.apply_array(res.w.array)
-    meta = dict(name=name, d=d, J=J, K=K, dist=dist, n_t=n_t, n_x=n_x,
+    meta = dict(name=name, d=d, J=J, K=K, dist=dist, n_t=n_t, n_x=n_x, domain=domain,
+                u0=u0_name(problem.u0),
                 D=np.asarray(problem.D, dtype=float).tolist(), c=float(problem.c),
                 seed_f=inputs.SEED_F, probe_seed=PROBE_SEED,
                 iterations=res.iterations, eps=eps, rho0=rho0,
@@ -150,16 +206,17 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.
           f"{meta['seconds']:.1f}s", flush=True)
 
 
-def mg_rows_case(name, d, K, rows=1):
+def mg_rows_case(name, d, K, rows=1, domain="square", D=None):
     """Full outputs of K_x (alpha=1, mu=0) and C_j (alpha=0.3, mu=2^j) MG
     applies on seeded rows at a larger K (streaming-kernel sizes)."""
-    hier = hw.build_mesh_hierarchy(d, K)
-    ops = hw.assemble_level_operators(hier)
+    hier = hw.build_mesh_hierarchy(d, K) if domain == "square" else lshape_hierarchy(K)
+    ops = hw.assemble_level_operators(hier, D)
     n = ops[-1].A_x.rows
     B = np.random.default_rng(PROBE_SEED).standard_normal((rows, n))
     arrays = dict()
     meta = dict(name=name, d=d, K=K, n=n, rows=rows, probe_seed=PROBE_SEED,
-                solvers=[])
+                solvers=[], domain=domain,
+                D=None if D is None else np.asarray(D, dtype=float).tolist())
     for (alpha, mu) in ((1.0, 0.0), (0.3, 2.0 ** 5), (0.3, 2.0 ** 10)):
         mg = hw.make_solver(hier, alpha, mu, 2, 3, level_operators=ops)
         X = np.empty_like(B)
@@ -238,6 +295,13 @@ CASES = {
     # anisotropic diffusion + reaction: |beta| = 0.43 along y > kRegBetaMax,
     # so the GPU multigrid takes the shared-ring (exact-scan) fallback
     "a1": lambda: run_case("a1", 2, 3, 6, "uniform", lean=True, D=[[1.0, 0.0], [0.0, 6.0]], c=0.5),
+    # mapped L-shaped domain (BASELINE cfg 5 recipe: D = I/4 after the map
+    # [-1,1]^2 -> [0,1]^2, F = 1 + U[-0.1, 0.1]); L1 also projects a
+    # non-zero u0, L2 uses cfg 5's u0 = 0 at register-kernel sizes
+    "L1": lambda: run_case("L1", 2, 3, 5, "lshape", D=0.25 * np.eye(2), domain="L",
+                           u0=inputs.u0_sines),
+    "L2": lambda: run_case("L2", 2, 4, 7, "lshape", lean=True, D=0.25 * np.eye(2), domain="L"),
+    "mgL8": lambda: mg_rows_case("mgL8", 2, 8, rows=2, domain="L", D=0.25 * np.eye(2)),
     "d2": lambda: run_case("d2", 1, 10, 10, "normal", full=False),
     "cfg2": lambda: run_case("cfg2", 2, 8, 8, "uniform", full=False),
     "mg8": lambda: mg_rows_case("mg8", 2, 8),
