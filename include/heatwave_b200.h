@@ -63,6 +63,22 @@ enum {
  *   L (off = 0.5, end = 0.5), T_test (1/sqrt h), N_test (sqrt h / 2,
  *   sqrt(3h)/6) -- see temporal.py:82-144.
  * wavelet_scale: J doubles, s_j = 2^(j/2) for j = 1..J (wavelet.py:63).
+ *
+ * domain (ABI v4): 0 = [0,1]^dim (the reference's meshes, spatial.py:98-137);
+ *   1 = the L-shaped domain of BASELINE config 5, [-1,1]^2 \ [0,1]^2 mapped
+ *   to [0,1]^2 \ [1/2,1]^2 (pass D = I/4 in coef / stencils; the mapped S,
+ *   f-hat are 1/4 and K_X 4x the unmapped ones, so PCG iterates agree).
+ *   Level l (h = 2^-l) has the vertices of the square's level l minus the
+ *   closed quadrant [1/2,1]^2; its dofs are the remaining interior vertices
+ *   in lexicographic order (x slow, y fast): N_x = (2^K-1)^2 - 4^(K-1).
+ *   The hierarchy starts at level 2 (5 dofs), inverted densely like the
+ *   reference's coarsest level (multigrid.py:118): coarse_inv holds
+ *   [(J + 2) operators][5][5] doubles (host), the inverse of the level-2
+ *   matrix alpha*A_2 + mu*M_2 of each operator in dof order.  Full contexts
+ *   take space-time arrays in the dof layout (rows of N_x); internally, and
+ *   in the time-slab entry points of kernel contexts (rows_max > 0), rows
+ *   use the embedded grid layout of (2^K-1)^2 points with the removed
+ *   quadrant held at zero -- hwg_grid_scatter / hwg_grid_gather convert.
  */
 typedef struct {
     int32_t dim;            /* 1 or 2 */
@@ -83,6 +99,9 @@ typedef struct {
      * buffers (hwg_schur_apply, hwg_kx_apply, hwg_rhs, hwg_wavelet, hwg_pcg
      * and hwg_solve_host then return HWG_EINVAL). */
     int64_t rows_max;
+    int32_t domain;         /* 0 square / cube, 1 L-shaped (dim 2, K in [2, 11]) */
+    int32_t reserved;
+    const double *coarse_inv;   /* domain 1: [(J + 2)][25] (host), else NULL */
 } hwg_desc;
 
 typedef struct hwg_ctx hwg_ctx;
@@ -225,6 +244,12 @@ int hwg_bt_rows(hwg_ctx *ctx, const double *G1, const double *G2, const double *
  * have 2*2^J test rows).  X must hold every row the band touches. */
 int hwg_temporal_rows(hwg_ctx *ctx, int band, const double *X, int64_t x0, double *Y, int64_t r0,
                       int64_t nr, void *stream);
+
+/* L-shaped domain: dof-layout rows (N_x values each) -> embedded grid rows
+ * ((2^K-1)^2 values, removed quadrant zero), and back.  For domain 0 both
+ * are plain copies. */
+int hwg_grid_scatter(hwg_ctx *ctx, const double *X, double *Y, int64_t rows, void *stream);
+int hwg_grid_gather(hwg_ctx *ctx, const double *X, double *Y, int64_t rows, void *stream);
 
 /* Batched V-cycles with a DEVICE array of per-row operator ids. */
 int hwg_mg_rows_dev(hwg_ctx *ctx, const int32_t *ops, const double *B, double *X, int64_t rows,

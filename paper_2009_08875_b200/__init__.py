@@ -7,7 +7,7 @@ hand-written sm_100a kernels in ``libhwgpu.so`` (C ABI:
 ``include/heatwave_b200.h``).  See DESIGN.md.
 """
 
-from .discretization import ProblemData
+from .discretization import ProblemData, lshape_problem
 from ._lib import IterationLimitError
 from .api import (SolveConfig, SpaceTimeVector, TemporalDiscretization, MeshHierarchy,
                   build_mesh_hierarchy, WaveletTransform, MultigridSolver, make_solver,

@@ -117,31 +117,36 @@ class TemporalDiscretization:
 
 
 class MeshHierarchy:
-    """Nested uniform meshes of [0,1]^d, levels 1..K (spatial.py:73-95)."""
+    """Nested uniform meshes of [0,1]^d, levels 1..K (spatial.py:73-95).
 
-    def __init__(self, d, K):
+    ``domain="L"``: the mapped L-shaped domain of BASELINE config 5
+    ([0,1]^2 minus [1/2,1]^2, levels 2..K; see discretization.lshape_problem)."""
+
+    def __init__(self, d, K, domain="square"):
         if d not in (1, 2, 3):
             raise ValueError("dimension must be 1, 2 or 3")
         if K < 1:
             raise ValueError("finest level K must be >= 1")
         if d == 3:
             raise NotImplementedError("the GPU path implements d = 1 and d = 2")
-        self.d, self.K = d, K
+        if domain not in ("square", "L") or (domain == "L" and (d != 2 or K < 2)):
+            raise ValueError("domain must be 'square' or 'L' (2D, K >= 2)")
+        self.d, self.K, self.domain = d, K, domain
         self._finest = None
 
     @property
     def finest(self) -> FineMesh:
         if self._finest is None:
-            self._finest = FineMesh(self.d, self.K)
+            self._finest = FineMesh(self.d, self.K, self.domain)
         return self._finest
 
     @property
     def N_x(self):
-        return (2 ** self.K - 1) ** self.d
+        return disc.lshape_dofs(self.K) if self.domain == "L" else (2 ** self.K - 1) ** self.d
 
 
-def build_mesh_hierarchy(d: int, K: int) -> MeshHierarchy:
-    return MeshHierarchy(d, K)
+def build_mesh_hierarchy(d: int, K: int, domain: str = "square") -> MeshHierarchy:
+    return MeshHierarchy(d, K, domain)
 
 
 def project_initial(mesh: FineMesh, u0):
@@ -270,6 +275,7 @@ def make_solver(hierarchy: MeshHierarchy, alpha: float, mu: float, n_vcycles: in
     if alpha <= 0 and mu <= 0:
         raise ValueError("need alpha > 0 or mu > 0")
     d, K = hierarchy.d, hierarchy.K
+    domain = getattr(hierarchy, "domain", "square")
     # every operator slot of this small (J = 1) context is (alpha, mu)
     table = np.zeros((3, K + 1, disc.COEF_STRIDE))
     for l in range(1, K + 1):
@@ -278,7 +284,9 @@ def make_solver(hierarchy: MeshHierarchy, alpha: float, mu: float, n_vcycles: in
         c0 = vals["c0"]
         table[:, l, :6] = [c0, vals["cx"], vals["cy"], vals["cd"], 1.0 / c0,
                            1.0 / c0 if l == 1 else 0.0]
-    ctx = GpuContext(d, 1, K, alpha, n_vcycles, n_smooth, D, c, device, coef=table)
+    cinv = disc.lshape_coarse_inverses([(alpha, mu)] * 3, D, c) if domain == "L" else None
+    ctx = GpuContext(d, 1, K, alpha, n_vcycles, n_smooth, D, c, device, coef=table,
+                     domain=domain, coarse_inv=cinv)
     return MultigridSolver(ctx, 0, alpha, mu, n_vcycles, n_smooth, hierarchy)
 
 
@@ -412,18 +420,20 @@ class ProblemAssembly:
 
 
 def assemble_system(problem: ProblemData, J: int, K: int, config: SolveConfig = None,
-                    forcing=None, host_rhs=True) -> ProblemAssembly:
+                    forcing=None, host_rhs=True, domain: str = "square") -> ProblemAssembly:
     """Assemble the GPU system (solver.py:353-386).
 
     Extensions: ``forcing`` -- nodal forcing values F (the BASELINE recipe);
-    ``host_rhs=False`` keeps f-hat on the device as a CUDA tensor."""
+    ``host_rhs=False`` keeps f-hat on the device as a CUDA tensor;
+    ``domain="L"`` -- the mapped L-shaped domain of BASELINE config 5
+    (problem from discretization.lshape_problem)."""
     config = config or SolveConfig()
     if config.exact_inverses:
         raise NotImplementedError("exact (sparse-LU) inner inverses stay on the CPU reference")
     d = problem.D.shape[0]
-    hier = build_mesh_hierarchy(d, K)
+    hier = build_mesh_hierarchy(d, K, domain)
     ctx = GpuContext(d, J, K, config.alpha, config.vcycles, config.smooth, problem.D,
-                     problem.c, config.device)
+                     problem.c, config.device, domain=domain)
     wt = WaveletTransform(ctx)
     K_x = MultigridSolver(ctx, 0, 1.0, 0.0, config.vcycles, config.smooth, hier)
     blocks = {j: MultigridSolver(ctx, 1 + j, config.alpha, 2.0 ** j, config.vcycles,
@@ -567,10 +577,10 @@ def measure_error(solution: HeatSolution, exact, t: float) -> float:
 
 
 def solve_heat(problem: ProblemData, J: int, K: int, config: SolveConfig = None,
-               forcing=None):
+               forcing=None, domain: str = "square"):
     """Assemble, run PCG, return (PCGResult, HeatSolution) (solver.py:389-403)."""
     config = config or SolveConfig()
-    asm = assemble_system(problem, J, K, config, forcing)
+    asm = assemble_system(problem, J, K, config, forcing, domain=domain)
     result = pcg(asm.S, asm.K_X, asm.rhs, config.epsilon, None, config.max_iterations,
                  config.recompute_every)
     u = asm.wavelet.apply_array(result.w.array)

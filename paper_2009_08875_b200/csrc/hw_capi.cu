@@ -56,7 +56,11 @@ struct hwg_ctx {
     hwg_desc d{};
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
-    int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx
+    int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
+    int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
+    int64_t nxu = 0, Nu = 0;           // dof-layout row length / size (= nx, N for domain 0)
+    double *cinv = nullptr;            // domain 1: [op][25] level-2 inverses (device)
+    double *Xg = nullptr, *Yg = nullptr;   // domain 1: grid-layout operands of full contexts
     int64_t rows_max = 0;              // MG batch capacity (rows)
     bool kernel_only = false;          // distributed-path context (no operator buffers)
     int64_t red_max = 0;               // capacity of the dot partial / tree scratch
@@ -282,7 +286,7 @@ static int64_t level_size(const hwg_ctx *c, int l)
 // last finest-level UP pass when that pass runs on mg2d_reg, else by row_dots
 static bool mg_dot_fusable(const hwg_ctx *c)
 {
-    return c->dim == 2 && c->K >= 6 && c->K <= 10 && c->mg_reg_ok;
+    return c->dim == 2 && c->K >= 6 && c->K <= 11 && c->mg_reg_ok;
 }
 
 static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op,
@@ -303,7 +307,8 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
             continue;
         }
         if (c->K <= kCoarseTop2d) {
-            MgCoarseArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, 1, ro, op, nr};
+            MgCoarseArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, 1, ro, op, nr,
+                           c->domain, c->cinv};
             ProfScope ps(c, st, 4, 16.0 * nr * c->nx);
             CK(mg2d_coarse_launch(a, st));
             ++c->launches;
@@ -326,6 +331,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.op = op;
                 a.zero_start = (l < c->K || cyc == 0) ? 1 : 0;
                 a.reg_ok = c->mg_reg_ok;
+                a.lshape = c->domain;
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
                 ProfScope ps(c, st, l == c->K ? 0 : 2,
                              8.0 * nr * (n2 * (a.zero_start ? 2 : 3) + m2));
@@ -334,7 +340,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
             }
             MgCoarseArgs ca{c->mgB[kCoarseTop2d], level_size(c, kCoarseTop2d),
                             c->mgX[kCoarseTop2d], level_size(c, kCoarseTop2d), c->coef,
-                            c->K + 1, kCoarseTop2d, 1, 1, ro, op, nr};
+                            c->K + 1, kCoarseTop2d, 1, 1, ro, op, nr, c->domain, c->cinv};
             {
                 ProfScope ps(c, st, 4, 16.0 * nr * level_size(c, kCoarseTop2d));
                 CK(mg2d_coarse_launch(ca, st));
@@ -355,6 +361,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.row_op = ro;
                 a.op = op;
                 a.reg_ok = c->mg_reg_ok;
+                a.lshape = c->domain;
                 if (fuse && l == c->K && cyc == c->nv - 1) {
                     a.dot_y = dot_y + r0 * c->nx;
                     a.dot_part = dot_part + r0;
@@ -373,10 +380,12 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
     return HWG_OK;
 }
 
+// column-wise, so any row layout works: nx = 0 means the grid layout
 static int wavelet(hwg_ctx *c, const double *X, double *Y, double *S1, double *S2, bool tr,
-                   cudaStream_t st)
+                   cudaStream_t st, int64_t nx = 0)
 {
-    CK(wavelet_apply(X, Y, S1, S2, c->J, c->scale.data(), c->nt, c->nx, tr, st, &c->launches));
+    CK(wavelet_apply(X, Y, S1, S2, c->J, c->scale.data(), c->nt, nx ? nx : c->nx, tr, st,
+                     &c->launches));
     return HWG_OK;
 }
 
@@ -411,6 +420,29 @@ static int kx(hwg_ctx *c, const double *X, double *Y, cudaStream_t st,
 
 static cudaStream_t S(void *s) { return (cudaStream_t)s; }
 
+// dof layout <-> grid layout (domain 1; plain copies otherwise)
+static int to_grid(hwg_ctx *c, const double *src, double *dst, int64_t rows, cudaStream_t st)
+{
+    if (!c->domain) {
+        if (src != dst) CK(cudaMemcpyAsync(dst, src, rows * c->nx * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return HWG_OK;
+    }
+    CK(launch_grid_scatter(src, dst, rows, c->grid, c->nxu, st));
+    ++c->launches;
+    return HWG_OK;
+}
+
+static int from_grid(hwg_ctx *c, const double *src, double *dst, int64_t rows, cudaStream_t st)
+{
+    if (!c->domain) {
+        if (src != dst) CK(cudaMemcpyAsync(dst, src, rows * c->nx * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return HWG_OK;
+    }
+    CK(launch_grid_gather(src, dst, rows, c->grid, c->nxu, st));
+    ++c->launches;
+    return HWG_OK;
+}
+
 static int ensure_pcg(hwg_ctx *c)
 {
     if (c->r) return HWG_OK;
@@ -427,7 +459,7 @@ static int ensure_pcg(hwg_ctx *c)
 extern "C" {
 
 const char *hwg_last_error(void) { return g_err.c_str(); }
-int hwg_version(void) { return 3; }
+int hwg_version(void) { return 4; }
 
 int hwg_create(const hwg_desc *desc, hwg_ctx **out)
 {
@@ -436,8 +468,12 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     const hwg_desc &d = *desc;
     if (d.dim != 1 && d.dim != 2) return fail(HWG_EINVAL, "dimension must be 1 or 2 on the GPU path");
     if (d.J < 1 || d.J > 24) return fail(HWG_EINVAL, "J must be in [1, 24]");
-    if (d.K < 1 || (d.dim == 2 && d.K > 10) || (d.dim == 1 && d.K > 10))
-        return fail(HWG_EINVAL, "K must be in [1, 10]");
+    if (d.domain != 0 && d.domain != 1) return fail(HWG_EINVAL, "unknown domain");
+    if (d.domain == 1 && d.dim != 2) return fail(HWG_EINVAL, "the L-shaped domain is 2D");
+    if (d.domain == 1 && (d.K < 2 || !d.coarse_inv))
+        return fail(HWG_EINVAL, "the L-shaped domain needs K >= 2 and the level-2 inverses");
+    if (d.K < 1 || (d.dim == 2 && d.K > 11) || (d.dim == 1 && d.K > 10))
+        return fail(HWG_EINVAL, d.dim == 2 ? "K must be in [1, 11]" : "K must be in [1, 10]");
     if (d.smooth != 3) return fail(HWG_EINVAL, "the GPU smoother is built for smooth = 3 sweeps");
     if (d.vcycles < 1) return fail(HWG_EINVAL, "vcycles must be >= 1");
     if (!d.coef || !d.stencil_M || !d.stencil_A || !d.temporal || !d.wavelet_scale)
@@ -453,9 +489,13 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     c->nt = (1LL << d.J) + 1;
     c->nx = d.dim == 2 ? (int64_t)c->m * c->m : c->m;
     c->N = c->nt * c->nx;
+    c->domain = d.domain;
+    const int lm = (c->m - 1) / 2;
+    c->nxu = d.domain ? c->nx - (int64_t)(c->m - lm) * (c->m - lm) : c->nx;
+    c->Nu = c->nt * c->nxu;
     c->rows_max = d.rows_max > 0 ? d.rows_max : 2 * c->nt;
     c->kernel_only = d.rows_max > 0;
-    c->grid = Grid{d.dim, c->m, c->nx};
+    c->grid = Grid{d.dim, c->m, c->nx, d.domain ? lm : (1 << 30)};
     c->SM = Stencil{d.stencil_M[0], d.stencil_M[1], d.stencil_M[2], d.stencil_M[3]};
     c->SA = Stencil{d.stencil_A[0], d.stencil_A[1], d.stencil_A[2], d.stencil_A[3]};
     c->scale.assign(d.wavelet_scale, d.wavelet_scale + d.J);
@@ -472,6 +512,12 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         if (ev[0] == '0') c->mg_reg_ok = 0;
         else if (ev[0] == '4' && c->mg_reg_ok) c->mg_reg_ok = 2;   // P = 4 at n = 1023
         else if (ev[0] == '5' && c->mg_reg_ok) c->mg_reg_ok = 3;   // P = 4 for UP at n = 1023
+    // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask
+    if (!c->mg_reg_ok && d.dim == 2 && d.K > kCoarseTop2d && (d.K > 10 || d.domain)) {
+        delete c;
+        return fail(HWG_EINVAL, "level operators with |c_y / c_0| > 0.2726 are supported on the "
+                                "square with K <= 10 only");
+    }
     int rc;
 #define GO(x)                      \
     do {                           \
@@ -482,6 +528,10 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         }                          \
     } while (0)
     GO(upload(c, &c->coef, c->coef_host));
+    if (c->domain) {
+        std::vector<double> ci(d.coarse_inv, d.coarse_inv + (size_t)nops * 25);
+        GO(upload(c, &c->cinv, ci));
+    }
     c->level_of.assign(c->nt, 0);
     for (int j = 1; j <= d.J; ++j)
         for (int64_t r = (1LL << (j - 1)) + 1; r <= (1LL << j); ++r) c->level_of[r] = j;
@@ -495,6 +545,10 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         GO(dalloc(c, &c->AxU, c->N));
         GO(dalloc(c, &c->T12, 2 * c->N));
         GO(dalloc(c, &c->G12, 2 * c->N));
+        if (c->domain) {
+            GO(dalloc(c, &c->Xg, c->N));
+            GO(dalloc(c, &c->Yg, c->N));
+        }
     }
     c->mgX.assign(d.K + 1, nullptr);
     c->mgB.assign(d.K + 1, nullptr);
@@ -567,16 +621,28 @@ int hwg_wavelet(hwg_ctx *c, const double *X, double *Y, int transpose, void *str
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (X == Y) return fail(HWG_EINVAL, "wavelet input and output may not alias");
-    TRY(wavelet(c, X, Y, c->T12, c->T12 + c->N, transpose != 0, S(stream)));
+    TRY(wavelet(c, X, Y, c->T12, c->T12 + c->N, transpose != 0, S(stream), c->nxu));
     return HWG_OK;
 }
 
 int hwg_spatial(hwg_ctx *c, int which, const double *X, double *Y, int64_t rows, void *stream)
 {
     if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
-    CK(launch_stencil_rows(X, which == 0 ? Y : nullptr, which == 0 ? nullptr : Y, c->grid,
-                           c->SM, c->SA, rows, S(stream)));
-    ++c->launches;
+    cudaStream_t st = S(stream);
+    if (!c->domain || c->kernel_only) {          // kernel contexts: grid layout
+        CK(launch_stencil_rows(X, which == 0 ? Y : nullptr, which == 0 ? nullptr : Y, c->grid,
+                               c->SM, c->SA, rows, st));
+        ++c->launches;
+        return HWG_OK;
+    }
+    for (int64_t r0 = 0; r0 < rows; r0 += 2 * c->nt) {   // dof layout via the T12 / G12 scratch
+        const int64_t nr = std::min<int64_t>(2 * c->nt, rows - r0);
+        TRY(to_grid(c, X + r0 * c->nxu, c->T12, nr, st));
+        CK(launch_stencil_rows(c->T12, which == 0 ? c->G12 : nullptr, which == 0 ? nullptr : c->G12,
+                               c->grid, c->SM, c->SA, nr, st));
+        ++c->launches;
+        TRY(from_grid(c, c->G12, Y + r0 * c->nxu, nr, st));
+    }
     return HWG_OK;
 }
 
@@ -584,7 +650,10 @@ int hwg_schur_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 {
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
-    return schur(c, X, Y, S(stream));
+    if (!c->domain) return schur(c, X, Y, S(stream));
+    TRY(to_grid(c, X, c->Xg, c->nt, S(stream)));
+    TRY(schur(c, c->Xg, c->Yg, S(stream)));
+    return from_grid(c, c->Yg, Y, c->nt, S(stream));
 }
 
 int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
@@ -592,7 +661,24 @@ int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (X == Y) return fail(HWG_EINVAL, "K_X input and output may not alias");
-    return kx(c, X, Y, S(stream));
+    if (!c->domain) return kx(c, X, Y, S(stream));
+    TRY(to_grid(c, X, c->Xg, c->nt, S(stream)));
+    TRY(kx(c, c->Xg, c->Yg, S(stream)));
+    return from_grid(c, c->Yg, Y, c->nt, S(stream));
+}
+
+int hwg_grid_scatter(hwg_ctx *c, const double *X, double *Y, int64_t rows, void *stream)
+{
+    if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    if (X == Y && c->domain) return fail(HWG_EINVAL, "layout conversion may not alias");
+    return to_grid(c, X, Y, rows, S(stream));
+}
+
+int hwg_grid_gather(hwg_ctx *c, const double *X, double *Y, int64_t rows, void *stream)
+{
+    if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
+    if (X == Y && c->domain) return fail(HWG_EINVAL, "layout conversion may not alias");
+    return from_grid(c, X, Y, rows, S(stream));
 }
 
 int hwg_mg_rows(hwg_ctx *c, int32_t op, const int32_t *op_host, const double *B, double *X,
@@ -601,15 +687,26 @@ int hwg_mg_rows(hwg_ctx *c, int32_t op, const int32_t *op_host, const double *B,
     if (!c || !B || !X || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
     if (op < 0 || op > c->J + 1) return fail(HWG_EKEY, "no multigrid operator " + std::to_string(op));
-    if (!op_host) return mg_apply(c, B, X, rows, op, nullptr, S(stream));
-    std::vector<int32_t> ops(op_host, op_host + rows);
-    for (int32_t o : ops)
-        if (o < 0 || o > c->J + 1) return fail(HWG_EKEY, "no multigrid operator " + std::to_string(o));
     int32_t *dops = nullptr;
-    CK(cudaMallocAsync((void **)&dops, std::max<int64_t>(rows, 1) * sizeof(int32_t), S(stream)));
-    CK(cudaMemcpyAsync(dops, ops.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice, S(stream)));
-    int rc = mg_apply(c, B, X, rows, 0, dops, S(stream));
-    cudaFreeAsync(dops, S(stream));
+    if (op_host) {
+        std::vector<int32_t> ops(op_host, op_host + rows);
+        for (int32_t o : ops)
+            if (o < 0 || o > c->J + 1) return fail(HWG_EKEY, "no multigrid operator " + std::to_string(o));
+        CK(cudaMallocAsync((void **)&dops, std::max<int64_t>(rows, 1) * sizeof(int32_t), S(stream)));
+        CK(cudaMemcpyAsync(dops, ops.data(), rows * sizeof(int32_t), cudaMemcpyHostToDevice, S(stream)));
+    }
+    int rc = HWG_OK;
+    if (!c->domain || c->kernel_only) {
+        rc = mg_apply(c, B, X, rows, op, dops, S(stream));
+    } else {                                   // dof layout via the T12 / G12 scratch
+        for (int64_t r0 = 0; r0 < rows && rc == HWG_OK; r0 += 2 * c->nt) {
+            const int64_t nr = std::min<int64_t>(2 * c->nt, rows - r0);
+            rc = to_grid(c, B + r0 * c->nxu, c->T12, nr, S(stream));
+            if (rc == HWG_OK) rc = mg_apply(c, c->T12, c->G12, nr, op, dops ? dops + r0 : nullptr, S(stream));
+            if (rc == HWG_OK) rc = from_grid(c, c->G12, X + r0 * c->nxu, nr, S(stream));
+        }
+    }
+    if (dops) cudaFreeAsync(dops, S(stream));
     return rc;
 }
 
@@ -620,6 +717,17 @@ int hwg_rhs(hwg_ctx *c, const double *F, const double *load, const double *u0pro
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     cudaStream_t st = S(stream);
     const int64_t nt = c->nt, nx = c->nx, N = c->N, ntest = 2 * (nt - 1);
+    double *const fout = fhat;
+    if (c->domain) {                       // dof-layout inputs -> grid layout
+        if (F) {
+            TRY(to_grid(c, F, c->Xg, nt, st));
+            F = c->Xg;
+        } else if (load) {
+            TRY(to_grid(c, load, c->T12, ntest, st));
+            load = c->T12;
+        }
+        fhat = c->Yg;
+    }
     // g part: W^T (T^T (x) M_x + N^T (x) A_x) K_Y y, y = (N (x) M_x) F
     if (F || load) {
         const double *y = load;
@@ -643,11 +751,12 @@ int hwg_rhs(hwg_ctx *c, const double *F, const double *load, const double *u0pro
     }
     if (u0proj) {
         CK(cudaMemsetAsync(c->T12, 0, N * sizeof(double), st));
-        CK(cudaMemcpyAsync(c->T12, u0proj, nx * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        TRY(to_grid(c, u0proj, c->T12, 1, st));
         TRY(wavelet(c, c->T12, c->G12, c->U, c->AxU, true, st));
         CK(launch_add(fhat, c->G12, fhat, N, st));
         ++c->launches;
     }
+    if (c->domain) TRY(from_grid(c, fhat, fout, nt, st));
     return HWG_OK;
 }
 
@@ -657,22 +766,22 @@ int hwg_dot(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *
     if (!c || !X || !Y || !result_host || rows < 0 || rows > c->rows_max)
         return fail(HWG_EINVAL, "bad argument");
     cudaStream_t st = S(stream);
-    CK(launch_dot(X, Y, rows, c->nx, c->part, c->tmp, c->scal + 8, st, &c->launches));
+    CK(launch_dot(X, Y, rows, c->kernel_only ? c->nx : c->nxu, c->part, c->tmp, c->scal + 8, st,
+                  &c->launches));
     CK(cudaMemcpyAsync(c->hscal + 8, c->scal + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *result_host = c->hscal[8];
     return HWG_OK;
 }
 
-int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
-            int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out, void *stream)
+}  // extern "C"
+
+// PCG on grid-layout f, w (hwg_pcg converts dof-layout operands)
+static int pcg_core(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
+                    int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out,
+                    cudaStream_t st)
 {
-    if (!c || !f || !w) return fail(HWG_EINVAL, "null argument");
-    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
-    if (!(epsilon > 0) && !(rtol > 0)) return fail(HWG_EINVAL, "tolerance must be positive");
-    if (max_iterations < 0 || recompute_every < 1) return fail(HWG_EINVAL, "bad iteration limits");
     TRY(ensure_pcg(c));
-    cudaStream_t st = S(stream);
     const int64_t N = c->N, nt = c->nt, nx = c->nx;
     hwg_pcg_stats dummy{};
     hwg_pcg_stats &out = st_out ? *st_out : dummy;
@@ -791,6 +900,28 @@ int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
     return fail(HWG_EMAXIT, buf);
 }
 
+extern "C" {
+
+int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
+            int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out, void *stream)
+{
+    if (!c || !f || !w) return fail(HWG_EINVAL, "null argument");
+    if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
+    if (!(epsilon > 0) && !(rtol > 0)) return fail(HWG_EINVAL, "tolerance must be positive");
+    if (max_iterations < 0 || recompute_every < 1) return fail(HWG_EINVAL, "bad iteration limits");
+    cudaStream_t st = S(stream);
+    if (!c->domain)
+        return pcg_core(c, f, w, epsilon, rtol, max_iterations, recompute_every, st_out, st);
+    TRY(to_grid(c, f, c->Xg, c->nt, st));
+    const int rc = pcg_core(c, c->Xg, c->Yg, epsilon, rtol, max_iterations, recompute_every,
+                            st_out, st);
+    if (rc != HWG_OK && rc != HWG_EMAXIT) return rc;
+    const std::string msg = g_err;
+    TRY(from_grid(c, c->Yg, w, c->nt, st));
+    if (rc != HWG_OK) g_err = msg;
+    return rc;
+}
+
 int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double epsilon,
                    double rtol, int32_t max_iterations, int32_t recompute_every,
                    hwg_pcg_stats *stats, void *stream)
@@ -798,16 +929,30 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
     if (!c || !fhat_host || !u_host) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     cudaStream_t st = S(stream);
+    if (!(epsilon > 0) && !(rtol > 0)) return fail(HWG_EINVAL, "tolerance must be positive");
+    if (max_iterations < 0 || recompute_every < 1) return fail(HWG_EINVAL, "bad iteration limits");
     if (!c->fdev) {
         TRY(dalloc(c, &c->fdev, c->N));
         TRY(dalloc(c, &c->wdev, c->N));
     }
-    CK(cudaMemcpyAsync(c->fdev, fhat_host, c->N * sizeof(double), cudaMemcpyHostToDevice, st));
-    int rc = hwg_pcg(c, c->fdev, c->wdev, epsilon, rtol, max_iterations, recompute_every, stats, stream);
+    CK(cudaMemcpyAsync(c->fdev, fhat_host, c->Nu * sizeof(double), cudaMemcpyHostToDevice, st));
+    const double *f = c->fdev;
+    if (c->domain) {                          // dof layout -> grid layout (in place is not
+        TRY(to_grid(c, c->fdev, c->Xg, c->nt, st));   // allowed: via Xg)
+        f = c->Xg;
+    }
+    int rc = pcg_core(c, f, c->wdev, epsilon, rtol, max_iterations, recompute_every, stats, st);
     if (rc != HWG_OK && rc != HWG_EMAXIT) return rc;
+    const std::string msg = g_err;
     TRY(wavelet(c, c->wdev, c->U, c->T12, c->T12 + c->N, false, st));
-    CK(cudaMemcpyAsync(u_host, c->U, c->N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    const double *u = c->U;
+    if (c->domain) {
+        TRY(from_grid(c, c->U, c->fdev, c->nt, st));
+        u = c->fdev;
+    }
+    CK(cudaMemcpyAsync(u_host, u, c->Nu * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (rc != HWG_OK) g_err = msg;
     return rc;
 }
 

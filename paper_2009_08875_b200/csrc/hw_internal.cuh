@@ -23,6 +23,7 @@ struct MgStreamArgs {
     int reg_ok;                         // |beta| small enough for mg2d_reg
     const double *dot_y;                // UP (mg2d_reg): dot_part[row] = <dot_y row, final X row>
     double *dot_part;
+    int lshape;                         // mapped L-shaped domain (mg2d_reg only)
 };
 
 struct MgCoarseArgs {
@@ -36,11 +37,13 @@ struct MgCoarseArgs {
     const int32_t *row_op;
     int op;
     int64_t rows;
+    int lshape;              // mapped L-shaped domain: masked quadrant, level-2 dense solve
+    const double *cinv;      // lshape: [op][25] inverse of the 5-dof level-2 operator
 };
 
 constexpr int kCoarseTop2d = 5;
 cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
-// register-resident variant (hw_mg2d_reg.cu), levels 6..10; cudaErrorNotSupported otherwise
+// register-resident variant (hw_mg2d_reg.cu), levels 6..11; cudaErrorNotSupported otherwise
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
 // largest |beta| = |cy / c0| mg2d_reg accepts (8-chunk window: |beta|^32 <= 2^-60)
 constexpr double kRegBetaMax = 0.2726;
@@ -79,6 +82,8 @@ struct Grid {
     int dim;
     int m;                 // points per direction
     int64_t nx;            // m^dim
+    int lm;                // 2D: points with i >= lm and j >= lm are masked (held at
+                           // zero; the L-shaped domain, lm = (m-1)/2), else > m
 };
 struct TCsr {              // temporal factor, CSR on the device
     const int32_t *ip, *ix;
@@ -103,6 +108,12 @@ cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *
                                int64_t nt, cudaStream_t st);
 cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
                        cudaStream_t st);
+// L-shaped domain: rows of the lexicographic dof layout (nxu per row) <-> the
+// embedded grid layout (g.nx per row, masked points zero)
+cudaError_t launch_grid_scatter(const double *src, double *dst, int64_t rows, Grid g, int64_t nxu,
+                                cudaStream_t st);
+cudaError_t launch_grid_gather(const double *src, double *dst, int64_t rows, Grid g, int64_t nxu,
+                               cudaStream_t st);
 cudaError_t launch_temporal_rows(TCsr B, const double *X, int64_t x0, double *Y, int64_t r0,
                                  int64_t nr, int64_t nx, cudaStream_t st);
 

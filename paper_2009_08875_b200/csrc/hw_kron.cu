@@ -40,6 +40,13 @@ __device__ __forceinline__ Pt point_of(const Grid &g)
     return p;
 }
 
+// L-shaped domain: the removed closed quadrant is not part of the dof set;
+// outputs there are zero (Grid::lm > m for the square, never masked)
+__device__ __forceinline__ bool masked_pt(const Pt &p, const Grid &g)
+{
+    return p.i >= g.lm && p.j >= g.lm;
+}
+
 __device__ __forceinline__ int64_t pidx(const Pt &p, const Grid &g)
 {
     return g.dim == 2 ? (int64_t)p.i * g.m + p.j : p.j;
@@ -125,10 +132,16 @@ __global__ void __launch_bounds__(TX * TY) stencil_rows(const double *__restrict
     if (!p.ok) return;
     const int k = (int)pidx(p, g);
     const bool in = interior_of(p, g);
+    const bool msk = masked_pt(p, g);
     for (int64_t r0 = (int64_t)blockIdx.z * kBtRows; r0 < rows; r0 += (int64_t)gridDim.z * kBtRows) {
         const int64_t r1 = r0 + kBtRows < rows ? r0 + kBtRows : rows;
         for (int64_t r = r0; r < r1; ++r) {
             const int64_t o = r * g.nx + k;
+            if (msk) {
+                if (YM) YM[o] = 0.0;
+                if (YA) YA[o] = 0.0;
+                continue;
+            }
             if (r + 2 < r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(X + o + 2 * g.nx));
             if (YM) YM[o] = stencil_at<DM>(X + o, p, g, in, M);
             if (YA) YA[o] = stencil_at<DA>(X + o, p, g, in, A);
@@ -149,10 +162,15 @@ __global__ void __launch_bounds__(TX * TY) bt_side(const double *__restrict__ G1
     if (!p.ok) return;
     const int k = (int)pidx(p, g);
     const bool in = interior_of(p, g);
+    const bool msk = masked_pt(p, g);
     for (int64_t r0 = (int64_t)blockIdx.z * kBtRows; r0 < rows; r0 += (int64_t)gridDim.z * kBtRows) {
         const int64_t r1 = r0 + kBtRows < rows ? r0 + kBtRows : rows;
         for (int64_t r = r0; r < r1; ++r) {
             const int64_t o = r * g.nx + k;
+            if (msk) {
+                out[o] = 0.0;
+                continue;
+            }
             if (r + 2 < r1) {
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(G1 + o + 2 * g.nx));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(G2 + o + 2 * g.nx));
@@ -198,8 +216,13 @@ __global__ void __launch_bounds__(TX * TY) bside_fused(const double *__restrict_
     if (!p.ok) return;
     const int k = (int)pidx(p, g);
     const bool in = interior_of(p, g);
+    const bool msk = masked_pt(p, g);
     const double *Uk = U + k;
     auto st = [&](int64_t c, double &mv, double &av) {
+        if (msk) {                                 // zero rows -> zero bands
+            mv = av = 0.0;
+            return;
+        }
         const double *x = Uk + (c - u0) * g.nx;
         mv = stencil_at<DM>(x, p, g, in, M);
         av = stencil_at<DA>(x, p, g, in, A);
@@ -282,6 +305,33 @@ __global__ void add_arrays(const double *__restrict__ X1, const double *__restri
         Y[e] = add_rn(X1[e], X2[e]);
 }
 
+// L-shaped domain layouts: dof row (lexicographic, grid row i holds n points
+// for i < lm and lm points after) <-> embedded grid row (masked points 0)
+__device__ __forceinline__ int64_t dof_offset(int i, const Grid &g)
+{
+    return i < g.lm ? (int64_t)i * g.m : (int64_t)g.lm * g.m + (int64_t)(i - g.lm) * g.lm;
+}
+
+__global__ void grid_scatter(const double *__restrict__ src, double *__restrict__ dst,
+                             int64_t rows, Grid g, int64_t nxu)
+{
+    const Pt p = point_of(g);
+    if (!p.ok) return;
+    const bool msk = masked_pt(p, g);
+    const int64_t k = pidx(p, g), ku = msk ? 0 : dof_offset(p.i, g) + p.j;
+    for (int64_t r = blockIdx.z; r < rows; r += gridDim.z)
+        dst[r * g.nx + k] = msk ? 0.0 : src[r * nxu + ku];
+}
+
+__global__ void grid_gather(const double *__restrict__ src, double *__restrict__ dst,
+                            int64_t rows, Grid g, int64_t nxu)
+{
+    const Pt p = point_of(g);
+    if (!p.ok || masked_pt(p, g)) return;
+    const int64_t k = pidx(p, g), ku = dof_offset(p.i, g) + p.j;
+    for (int64_t r = blockIdx.z; r < rows; r += gridDim.z) dst[r * nxu + ku] = src[r * g.nx + k];
+}
+
 static unsigned grid_for(int64_t total, int bs)
 {
     int64_t g = (total + bs - 1) / bs;
@@ -356,6 +406,22 @@ cudaError_t launch_temporal_rows(TCsr B, const double *X, int64_t x0, double *Y,
     if (nr <= 0) return cudaSuccess;
     dim3 grid((unsigned)((nx + 255) / 256), (unsigned)(nr < 65535 ? nr : 65535));
     temporal_rows<<<grid, 256, 0, st>>>(B, X, x0, Y, r0, nr, nx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid_scatter(const double *src, double *dst, int64_t rows, Grid g, int64_t nxu,
+                                cudaStream_t st)
+{
+    if (rows <= 0) return cudaSuccess;
+    grid_scatter<<<spatial_grid(g, rows), dim3(TX, TY), 0, st>>>(src, dst, rows, g, nxu);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grid_gather(const double *src, double *dst, int64_t rows, Grid g, int64_t nxu,
+                               cudaStream_t st)
+{
+    if (rows <= 0) return cudaSuccess;
+    grid_gather<<<spatial_grid(g, rows), dim3(TX, TY), 0, st>>>(src, dst, rows, g, nxu);
     return cudaGetLastError();
 }
 

@@ -432,11 +432,23 @@ struct Cf {
     HW_DEV Cf(const double *c) : c0(c[kC0]), cx(c[kCx]), cy(c[kCy]), cd(c[kCd]), diag(c[kCd] != 0.0) {}
 };
 
+// L-shaped domain (LSH): point (i, j) of level L lies in the removed closed
+// quadrant -- not a dof, held at zero.  An unmasked point's neighbours in the
+// quadrant contribute exact zeros, and they come last in its CSR row (they
+// are "upper" neighbours), so the CSR-order arithmetic is unchanged.
+template <int L, bool LSH>
+__device__ __forceinline__ bool masked(int i, int j)
+{
+    constexpr int h = (Lc<L>::m - 1) / 2;
+    return LSH && i >= h && j >= h;
+}
+
 // one point update in CSR column order (the reference's arithmetic)
-template <int L>
+template <int L, bool LSH>
 __device__ __forceinline__ void gs_point(double *x, const double *b, const Cf &c, int i, int j)
 {
     constexpr int m = Lc<L>::m, p = Lc<L>::pitch;
+    if (masked<L, LSH>(i, j)) return;
     const int k = i * p + j;
     double acc = b[k];
     if (i > 0 && j > 0 && c.diag) acc = sub_mul(acc, c.cd, x[k - p - 1]);
@@ -458,7 +470,7 @@ __device__ __forceinline__ void gs_point(double *x, const double *b, const Cf &c
 // so every point sees exactly the operands of three sequential sweeps
 // (bit-identical), in 2m+5 steps instead of 3(2m-1).  m <= 31: one grid row
 // per lane.
-template <int L>
+template <int L, bool LSH>
 __device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, const Cf &c,
                                               bool forward, int lane)
 {
@@ -476,25 +488,46 @@ __device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, cons
             const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
             const int ihi = d < m - 1 ? d : m - 1;
             const int i = ilo + lane;
-            if (i <= ihi) gs_point<L>(x, b, c, i, d - i);
+            if (i <= ihi) gs_point<L, LSH>(x, b, c, i, d - i);
         }
         __syncwarp();
     }
 }
 
-template <int L>
+// the 5 dofs of the L's level 2 (3 x 3 grid, pitch 4): (0,0) (0,1) (0,2)
+// (1,0) (2,0) in lexicographic order
+__device__ __forceinline__ int lsh_dof2(int a) { return a < 3 ? a : (a - 2) * 4; }
+
+template <int L, bool LSH>
 __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw,
-                                              const double *coef, int lane)
+                                              const double *coef, const double *cinv, int lane)
 {
-    if constexpr (L >= 2) {
+    if constexpr (LSH && L == 2) {
+        // the L's coarsest level: dense inverse (multigrid.py:118,
+        // _kernels.py:168-173: acc += inv[i, j] * b[j] in column order)
+        double *x = xw + Lc<2>::off;
+        const double *b = bw + Lc<2>::off;
+        double acc = 0.0;
+        if (lane < 5) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) acc = add_mul(acc, cinv[lane * 5 + q], b[lsh_dof2(q)]);
+        }
+        __syncwarp();
+        if (lane < 5) x[lsh_dof2(lane)] = acc;
+        __syncwarp();
+    } else if constexpr (L >= 2) {
         constexpr int m = Lc<L>::m, p = Lc<L>::pitch, mc = Lc<L - 1>::m, pc = Lc<L - 1>::pitch;
         const double *c = coef + L * kCoefStride;
         const Cf cf(c);
-        coarse_sweep3<L>(xw, bw, cf, true, lane);
+        coarse_sweep3<L, LSH>(xw, bw, cf, true, lane);
         double *x = xw + Lc<L>::off;
         const double *b = bw + Lc<L>::off;
         for (int k = lane; k < m * m; k += 32) {           // residual
             const int i = k / m, j = k % m, q = i * p + j;
+            if (masked<L, LSH>(i, j)) {
+                rw[q] = 0.0;
+                continue;
+            }
             double acc = b[q];
             if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[q - p - 1]);
             if (i > 0) acc = sub_mul(acc, c[kCx], x[q - p]);
@@ -519,11 +552,11 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
             acc = add_mul(acc, 0.5, r1[2]);
             acc = add_mul(acc, 0.5, r2[1]);
             acc = add_mul(acc, 0.5, r2[2]);
-            bc[I * pc + J] = acc;
+            bc[I * pc + J] = masked<L - 1, LSH>(I, J) ? 0.0 : acc;
             xc[I * pc + J] = 0.0;
         }
         __syncwarp();
-        coarse_vcycle<L - 1>(xw, bw, rw, coef, lane);
+        coarse_vcycle<L - 1, LSH>(xw, bw, rw, coef, cinv, lane);
         const double *xcc = xw + Lc<L - 1>::off;
         for (int k = lane; k < m * m; k += 32) {           // prolongate (spatial.py:140-173)
             const int gi = k / m + 1, gj = k % m + 1;      // 1-based fine grid coords
@@ -542,17 +575,17 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
                 if (!(bi < 1 || bj < 1 || bi > mc || bj > mc)) acc = add_mul(acc, 0.5, cv(bi, bj));
             }
             const int q = (gi - 1) * p + (gj - 1);
-            x[q] = add_rn(x[q], acc);
+            if (!masked<L, LSH>(gi - 1, gj - 1)) x[q] = add_rn(x[q], acc);
         }
         __syncwarp();
-        coarse_sweep3<L>(xw, bw, cf, false, lane);
+        coarse_sweep3<L, LSH>(xw, bw, cf, false, lane);
     } else {
         if (lane == 0) xw[0] = add_mul(0.0, coef[1 * kCoefStride + kCoarse], bw[0]);  // 1x1 solve
         __syncwarp();
     }
 }
 
-template <int TOP, int WPB>
+template <int TOP, int WPB, bool LSH>
 __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, int64_t row, int lane)
 {
     constexpr int m = Lc<TOP>::m, p = Lc<TOP>::pitch;
@@ -568,11 +601,12 @@ __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, in
         xw[q] = a.zero_start ? 0.0 : Xg[k];
     }
     __syncwarp();
-    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP>(xw, bw, rw, coef, lane);
+    const double *cinv = LSH ? a.cinv + (int64_t)op * 25 : nullptr;
+    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP, LSH>(xw, bw, rw, coef, cinv, lane);
     for (int k = lane; k < m * m; k += 32) Xg[k] = xw[Lc<TOP>::off + (k / m) * p + k % m];
 }
 
-template <int WPB>
+template <int WPB, bool LSH>
 __global__ void __launch_bounds__(32 * WPB) mg2d_coarse(MgCoarseArgs a)
 {
     extern __shared__ double sm[];
@@ -581,11 +615,11 @@ __global__ void __launch_bounds__(32 * WPB) mg2d_coarse(MgCoarseArgs a)
     if (row >= a.rows) return;
     double *xw = sm + (size_t)w * kCoarseWords;
     switch (a.top) {
-    case 1: coarse_row<1, WPB>(a, xw, row, lane); break;
-    case 2: coarse_row<2, WPB>(a, xw, row, lane); break;
-    case 3: coarse_row<3, WPB>(a, xw, row, lane); break;
-    case 4: coarse_row<4, WPB>(a, xw, row, lane); break;
-    default: coarse_row<5, WPB>(a, xw, row, lane); break;
+    case 1: if constexpr (!LSH) coarse_row<1, WPB, LSH>(a, xw, row, lane); break;
+    case 2: coarse_row<2, WPB, LSH>(a, xw, row, lane); break;
+    case 3: coarse_row<3, WPB, LSH>(a, xw, row, lane); break;
+    case 4: coarse_row<4, WPB, LSH>(a, xw, row, lane); break;
+    default: coarse_row<5, WPB, LSH>(a, xw, row, lane); break;
     }
 }
 
@@ -613,6 +647,7 @@ cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, c
         const cudaError_t e = mg2d_reg_launch(a, down, rows, st);
         if (e != cudaErrorNotSupported) return e;
     }
+    if (a.lshape) return cudaErrorNotSupported;   // masked levels: mg2d_reg only
     if (n <= 96)
         return down ? launch_stream_t<3, 32, true>(a, rows, st) : launch_stream_t<3, 32, false>(a, rows, st);
     if (n <= 160)
@@ -630,7 +665,7 @@ cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st)
 {
     constexpr int WPB = 4;
     const size_t smem = (size_t)WPB * kCoarseWords * sizeof(double);
-    auto k = mg2d_coarse<WPB>;
+    auto k = a.lshape ? mg2d_coarse<WPB, true> : mg2d_coarse<WPB, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((a.rows + WPB - 1) / WPB);

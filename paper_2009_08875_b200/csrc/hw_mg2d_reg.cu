@@ -1,5 +1,5 @@
 // hw_mg2d_reg.cu -- register-resident streamed multigrid level passes, 2D,
-// levels l = 6..10 (n = 2^l - 1 = P NT - 1 points per direction).
+// levels l = 6..11 (n = 2^l - 1 = P NT - 1 points per direction).
 //
 // Same operator as mg2d_stream (hw_mg2d.cu; the reference's _mg_core,
 // /root/reference/pkg/src/heatwave/_kernels.py:110-199): per temporal row,
@@ -32,6 +32,15 @@
 //    zero-filling cp.async into THREAD-PRIVATE shared-memory slots three
 //    steps ahead, so they need no barrier; each step has two barriers
 //    (halo exchange, carry exchange).
+//  * LSH: the mapped L-shaped domain, embedded in the square grid with the
+//    closed quadrant i, j >= m = (n-1)/2 (natural coordinates) held at zero.
+//    Lexicographic GS on the L is GS on the square with those points reset
+//    to zero: the recurrence restarts (y = 0) at a masked point, so masked
+//    chunk ends are zero and carry nothing into the next unmasked chunk, and
+//    the final values of masked points are forced to zero after the carry
+//    (DOWN: the masked part of a row is a suffix; UP, point-reversed, a
+//    prefix).  Masked residuals are zero before restriction; prolongation
+//    needs nothing (masked fine points interpolate masked coarse zeros).
 #include "hw_common.cuh"
 #include "hw_internal.cuh"
 
@@ -80,7 +89,7 @@ struct RegSmem {
 
 // LB0 / LX0 (UP only): layout parity of grid row 0 of b / x0 (stage_row);
 // row i has parity L0 ^ (i & 1) because a grid row is n (odd) words long
-template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0>
+template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0, bool LSH>
 struct RegPass {
     static constexpr int NW = NT / 32;
     static constexpr int n = P * NT - 1;
@@ -115,6 +124,7 @@ struct RegPass {
     int sb, sx;                           // ring slots of b(t) and x0(t+1) at step t
     int sc;                               // UP: ring slot of coarse row floor(t/2) at step t
     double HC[NC];                        // UP: 0.5 x the latest coarse row this thread reads
+    unsigned cm;                          // LSH: bit k = column P t + k lies in the masked range
     // column tid + k NT sits at cpo + k NT when the swizzle is periodic in NT
     static constexpr bool LIN = (NT / 16) % (P / 2) == 0;
 
@@ -183,6 +193,12 @@ struct RegPass {
         for (int k = tid; k < SM::total; k += NT) sm[k] = 0.0;   // pads stay zero
         cpo = phys(tid);
         hoff = phys(P * (tid + 1));
+        cm = 0u;
+        if constexpr (LSH) {
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+                if (DOWN ? (P * tid + k >= m) : (P * tid + k <= m)) cm |= 1u << k;
+        }
 #pragma unroll
         for (int h = 0; h <= P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
         sb = 4;                                // step -3 (the prologue's first group)
@@ -423,9 +439,19 @@ struct RegPass {
         }
     }
 
+    // LSH: mask bits of grid row i (DOWN: rows >= m mask columns >= m; UP,
+    // point-reversed: rows <= m mask columns <= m)
+    HW_DEV unsigned rmask(int i) const
+    {
+        if constexpr (!LSH) return 0u;
+        return (DOWN ? i >= m : i <= m) ? cm : 0u;
+    }
+
     // zero-carry chunk recurrence of one sweep over the thread's P points
+    // (masked points, bits of rm, restart it at zero)
     HW_DEV void chunk(const double u[P], double uL, const double c[P], double cR,
-                      const double d[P], double dR, const double b[P], double y[P]) const
+                      const double d[P], double dR, const double b[P], double y[P],
+                      unsigned rm) const
     {
         double yy = 0.0;
 #pragma unroll
@@ -437,6 +463,7 @@ struct RegPass {
             const double e2 = u[k] + d[k];
             const double e3 = fma(cd, dr, cy * cr);
             yy = fma(beta, yy, (fma(-cx, e2, e1) - e3) * inv);
+            if (LSH && ((rm >> k) & 1u)) yy = 0.0;
             y[k] = yy;
         }
     }
@@ -469,6 +496,7 @@ struct RegPass {
 
         // ---- phase A: chunk recurrences of the three sweeps ----
         double y[3][P], b[P + 1];
+        const unsigned rm0 = rmask(t), rm1 = rmask(t - 2), rm2 = rmask(t - 4);
         constexpr int LBr = LB0 ^ PAR, LXr = LX0 ^ PAR ^ 1;   // UP parities of b(t), x0(t+1)
         double dn0[P + 1];
         if constexpr (DOWN && ZS) {
@@ -476,16 +504,16 @@ struct RegPass {
 #pragma unroll
             for (int k = 0; k < P; ++k) z[k] = 0.0;
             load_b<LBr>(0, b);
-            chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0]);
+            chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0], rm0);
         } else {
             load_x0<Q, EDGE, LXr>(t + 1, sx, sc, dn0);
             load_b<LBr>(0, b);
-            chunk(X1[Q], X1L, X0n, X0n[P], dn0, dn0[P], b, y[0]);
+            chunk(X1[Q], X1L, X0n, X0n[P], dn0, dn0[P], b, y[0], rm0);
         }
         load_b<LBr>(2, b);
-        chunk(X2[Q], X2L, X1[PAR], X1R[PAR], X1[Q], X1R[Q], b, y[1]);
+        chunk(X2[Q], X2L, X1[PAR], X1R[PAR], X1[Q], X1R[Q], b, y[1], rm1);
         load_b<LBr>(4, b);
-        chunk(X3, X3L, X2[PAR], X2R[PAR], X2[Q], X2R[Q], b, y[2]);
+        chunk(X3, X3L, X2[PAR], X2R[PAR], X2[Q], X2R[Q], b, y[2], rm2);
 
         // residual of grid row t-6 from d(t-6), d(t-5)
         double R[P];
@@ -495,6 +523,12 @@ struct RegPass {
                 const double d6r = k < P - 1 ? D[PAR][k + 1] : DR[PAR];
                 const double d5r = k < P - 1 ? D[Q][k + 1] : DR[Q];
                 R[k] = fma(-cy, d6r, fma(-cx, D[Q][k], -cd * d5r));
+            }
+            if constexpr (LSH) {
+                const unsigned rr = rmask(t - 6);
+#pragma unroll
+                for (int k = 0; k < P; ++k)
+                    if ((rr >> k) & 1u) R[k] = 0.0;
             }
             if (lane == 0) HRes[warp] = R[0];
         }
@@ -517,10 +551,11 @@ struct RegPass {
             const double prev = __shfl_up_sync(0xffffffffu, A[s], 1);
             cin[s] = fma(gl, tot[s * HS + warp], lane ? prev : 0.0);
             const bool vs = s == 0 ? v1 : (s == 1 ? v2 : v3);
+            const unsigned rms = s == 0 ? rm0 : (s == 1 ? rm1 : rm2);
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 const double v = fma(bp[k], cin[s], y[s][k]);
-                xn[s][k] = (vs && !(k == P - 1 && last)) ? v : 0.0;
+                xn[s][k] = (vs && !(k == P - 1 && last) && !(LSH && ((rms >> k) & 1u))) ? v : 0.0;
             }
             if (!vs) cin[s] = 0.0;
         }
@@ -636,20 +671,20 @@ struct RegPass {
     }
 };
 
-template <int P, int NT, bool DOWN, bool ZS, int LB, int LX>
+template <int P, int NT, bool DOWN, bool ZS, int LB, int LX, bool LSH>
 HW_DEV void run_pass(const MgStreamArgs &a, double *sm)
 {
-    RegPass<P, NT, DOWN, ZS, LB, LX> p(a, sm);
+    RegPass<P, NT, DOWN, ZS, LB, LX, LSH> p(a, sm);
     p.run();
     p.finish_dot(a);
 }
 
-template <int P, int NT, bool DOWN, bool ZS, int MINB>
+template <int P, int NT, bool DOWN, bool ZS, int MINB, bool LSH>
 __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
 {
     extern __shared__ __align__(16) double sm[];
     if constexpr (DOWN) {
-        run_pass<P, NT, DOWN, ZS, 0, 0>(a, sm);
+        run_pass<P, NT, DOWN, ZS, 0, 0, LSH>(a, sm);
     } else {
         // UP: layout parity of grid row 0 (stage_row) = 1 when local column 0
         // (global row n-1, column n-1) sits at a 16-byte boundary
@@ -661,11 +696,11 @@ __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
         };
         const int lb = parity(a.B, a.ldB), lx = parity(a.X, a.ldX);
         if (lb) {
-            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1>(a, sm);
-            else run_pass<P, NT, DOWN, ZS, 1, 0>(a, sm);
+            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1, LSH>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 1, 0, LSH>(a, sm);
         } else {
-            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1>(a, sm);
-            else run_pass<P, NT, DOWN, ZS, 0, 0>(a, sm);
+            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1, LSH>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 0, 0, LSH>(a, sm);
         }
     }
 }
@@ -674,7 +709,7 @@ template <int P, int NT, bool DOWN, bool ZS, int MINB>
 cudaError_t launch_reg_t(const MgStreamArgs &a, int64_t rows, cudaStream_t st)
 {
     const size_t smem = RegSmem<P, NT, DOWN, ZS>::total * sizeof(double);
-    auto k = mg2d_reg<P, NT, DOWN, ZS, MINB>;
+    auto k = a.lshape ? mg2d_reg<P, NT, DOWN, ZS, MINB, true> : mg2d_reg<P, NT, DOWN, ZS, MINB, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)rows, NT, smem, st>>>(a);
@@ -702,6 +737,7 @@ cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cuda
         // HWG_MG_REG=4: P = 4 for both passes; =5: P = 4 for UP only (A/B)
         if (a.reg_ok == 2 || (a.reg_ok == 3 && !down)) return launch_reg_n<4, 256, 1>(a, down, rows, st);
         return launch_reg_n<8, 128, 2>(a, down, rows, st);
+    case 2047: return launch_reg_n<8, 256, 1>(a, down, rows, st);
     default: return cudaErrorNotSupported;
     }
 }

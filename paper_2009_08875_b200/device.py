@@ -53,16 +53,25 @@ class GpuContext:
     """Owns one hwg_ctx: tables, workspaces and the launch counter."""
 
     def __init__(self, d, J, K, alpha=0.3, vcycles=2, smooth=3, D=None, c=0.0,
-                 device=0, coef=None, rows_max=0):
+                 device=0, coef=None, rows_max=0, domain="square", coarse_inv=None):
+        if domain not in ("square", "L"):
+            raise ValueError("domain must be 'square' or 'L'")
         self.device = require_cuda(device)
         self.lib = _lib.load()
         self.d, self.J, self.K = d, J, K
         self.alpha = alpha
+        self.domain = domain
         self.n_t = 2 ** J + 1
         self.m = 2 ** K - 1
-        self.n_x = self.m ** d
+        self.n_grid = self.m ** d                     # points per row of the grid layout
+        self.n_x = disc.lshape_dofs(K) if domain == "L" else self.n_grid
         self.coef = np.ascontiguousarray(
             disc.coef_table(d, J, K, alpha, D, c) if coef is None else coef, dtype=np.float64)
+        self.coarse_inv = None
+        if domain == "L":
+            self.coarse_inv = np.ascontiguousarray(
+                disc.lshape_coarse_inverses(disc.operator_list(J, alpha), D, c)
+                if coarse_inv is None else coarse_inv, dtype=np.float64)
         Mf, Af = disc.level_stencils(d, K, D, c)
         self.stencil_M = disc.stencil_vector(Mf, d)
         self.stencil_A = disc.stencil_vector(Af, d)
@@ -73,7 +82,9 @@ class GpuContext:
                             coef=self.coef.ctypes.data, stencil_M=self.stencil_M.ctypes.data,
                             stencil_A=self.stencil_A.ctypes.data,
                             temporal=self.temporal.ctypes.data,
-                            wavelet_scale=self.scales.ctypes.data, rows_max=int(rows_max))
+                            wavelet_scale=self.scales.ctypes.data, rows_max=int(rows_max),
+                            domain=1 if domain == "L" else 0,
+                            coarse_inv=self.coarse_inv.ctypes.data if self.coarse_inv is not None else None)
         h = C.c_void_p()
         _lib.check(self.lib.hwg_create(C.byref(desc), C.byref(h)))
         self.handle = h
@@ -137,6 +148,14 @@ class GpuContext:
     def temporal_rows(self, band, X, x0, Y, r0, nr):
         _lib.check(self.lib.hwg_temporal_rows(self.handle, self.BANDS[band], ptr(X), x0, ptr(Y),
                                               r0, nr, self.stream()))
+
+    def grid_scatter(self, X, Y):
+        """dof-layout rows X -> grid-layout rows Y (L-shaped domain)."""
+        _lib.check(self.lib.hwg_grid_scatter(self.handle, ptr(X), ptr(Y), X.shape[0], self.stream()))
+
+    def grid_gather(self, X, Y):
+        """grid-layout rows X -> dof-layout rows Y."""
+        _lib.check(self.lib.hwg_grid_gather(self.handle, ptr(X), ptr(Y), X.shape[0], self.stream()))
 
     def mg_rows_dev(self, ops, B, X):
         _lib.check(self.lib.hwg_mg_rows_dev(self.handle, ptr(ops), ptr(B), ptr(X), B.shape[0],

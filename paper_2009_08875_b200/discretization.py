@@ -70,6 +70,52 @@ def _grid_mesh(d, cells, h):
     return verts, np.concatenate([first, second])
 
 
+def _lshape_filter(elems, cells):
+    """Drop the elements of the removed quadrant [1/2,1]^2 from a square
+    mesh of ``cells`` x ``cells`` cells (element order otherwise kept: the
+    first half are the (i,j),(i+1,j),(i+1,j+1) triangles, the second half
+    the (i,j),(i+1,j+1),(i,j+1) ones, both over cells (a, b) in ij order)."""
+    g = np.arange(cells)
+    a, b = (t.ravel() for t in np.meshgrid(g, g, indexing="ij"))
+    keep = ~((a >= cells // 2) & (b >= cells // 2))
+    return np.concatenate([elems[: cells * cells][keep], elems[cells * cells:][keep]])
+
+
+def lshape_interior(gi, n):
+    """Interior vertices of the mapped L (grid coordinates gi, n cells)."""
+    return np.all((gi > 0) & (gi < n), axis=1) & ~np.all(gi >= n // 2, axis=1)
+
+
+def lshape_dofs(K):
+    """N_x of the mapped L at level K: (2^K-1)^2 - 4^(K-1)."""
+    return (2 ** K - 1) ** 2 - 4 ** (K - 1)
+
+
+def lshape_coarse_inverses(ops, D=None, c=0.0):
+    """[(len(ops)), 25]: scipy.linalg.inv of alpha*A_2 + mu*M_2 on the L's
+    5-dof level 2, per operator (alpha, mu) -- make_solver's coarse_inv
+    (multigrid.py:98-118) for the reference hierarchy of the L, assembled
+    like assemble_spatial (spatial.py:202-229)."""
+    import scipy.linalg as sla
+    D = np.eye(2) if D is None else np.atleast_2d(np.asarray(D, dtype=float))
+    verts, elems = _grid_mesh(2, 4, 0.25)
+    elems = _lshape_filter(elems, 4)
+    locM, locA = _element_matrices(verts, elems, 2, D, c)
+    gi = np.rint(verts * 4).astype(int)
+    inner = np.nonzero(lshape_interior(gi, 4))[0]
+    mats = []
+    for loc in (locM, locA):
+        A = _assembled(verts, elems, loc)[inner][:, inner].tocsr()
+        mats.append(((A + A.T) / 2).tocsr())
+    Mx, Ax = mats
+    out = np.zeros((len(ops), 25))
+    for o, (a, mu) in enumerate(ops):
+        S = a * Ax + mu * Mx
+        S.sort_indices()
+        out[o] = np.ascontiguousarray(sla.inv(S.tocsr().toarray())).ravel()
+    return out
+
+
 def _element_matrices(verts, elems, d, D, c):
     v = verts[elems]
     E = v[:, 1:, :] - v[:, :1, :]
@@ -195,18 +241,27 @@ _QUAD = {
 
 
 class FineMesh:
-    """The finest level's mesh with its interior numbering."""
+    """The finest level's mesh with its interior numbering.
 
-    def __init__(self, d, K):
+    ``domain="L"``: the mapped L-shaped domain [0,1]^2 minus [1/2,1]^2 (the
+    square's vertices and element order, removed-quadrant cells dropped)."""
+
+    def __init__(self, d, K, domain="square"):
         if d not in (1, 2):
             raise ValueError("the GPU path supports d = 1, 2")
-        self.d, self.K = d, K
+        if domain not in ("square", "L") or (domain == "L" and d != 2):
+            raise ValueError("domain must be 'square' or (2D) 'L'")
+        self.d, self.K, self.domain = d, K, domain
         n = 2 ** K
         verts, elems = _grid_mesh(d, n, 1.0)
         self.vertices = verts / n
-        self.elements = elems
         gi = np.rint(self.vertices * n).astype(int)
-        self.interior = np.nonzero(np.all((gi > 0) & (gi < n), axis=1))[0]
+        if domain == "L":
+            self.elements = _lshape_filter(elems, n)
+            self.interior = np.nonzero(lshape_interior(gi, n))[0]
+        else:
+            self.elements = elems
+            self.interior = np.nonzero(np.all((gi > 0) & (gi < n), axis=1))[0]
 
     @property
     def n_interior(self):
@@ -268,3 +323,15 @@ def l2_error_on_mesh(mesh: FineMesh, coeffs, exact) -> float:
     ue = np.asarray(exact(pts.reshape(-1, mesh.d))).reshape(uh.shape)
     err2 = np.einsum("eq,q->e", (uh - ue) ** 2, w) * vol
     return float(np.sqrt(err2.sum()))
+
+
+def lshape_problem(u0=None, g=None, c=0.0):
+    """BASELINE cfg 5 in the mapped coordinates the GPU path uses.
+
+    u_t - Laplace u = f on [-1,1]^2 minus [0,1]^2 becomes, under x -> (x+1)/2,
+    u_t - div(D grad u) = f on [0,1]^2 minus [1/2,1]^2 with D = I/4.  In 2D
+    the mapped M_x is 1/4 of the original and A_x (D = I/4) too, so the
+    mapped S-hat and f-hat are 1/4 and K_X 4x the original ones: PCG
+    iterates, iteration counts and the rtol stopping rule are unchanged."""
+    zero = lambda pts: np.zeros(len(pts))  # noqa: E731
+    return ProblemData(D=0.25 * np.eye(2), c=c, u0=u0 if u0 is not None else zero, g=g)

@@ -24,11 +24,14 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2009_08875_b200 as hw  # noqa: E402
 from paper_2009_08875_b200 import inputs  # noqa: E402
 
-FULL_CASES = ("c1", "d1", "c2s", "a1")
+FULL_CASES = ("c1", "d1", "c2s", "a1", "L1", "L2")
 
 
 def _problem(meta):
-    u0 = inputs.u0_sines if meta["dist"] == "uniform" else inputs.u0_modes()
+    if "u0" in meta:
+        u0 = inputs.u0_by_name(meta["u0"])
+    else:
+        u0 = inputs.u0_sines if meta["dist"] == "uniform" else inputs.u0_modes()
     D = np.asarray(meta["D"]) if "D" in meta else np.eye(meta["d"])
     return hw.ProblemData(D=D, c=meta.get("c", 0.0), u0=u0)
 
@@ -37,17 +40,20 @@ def _problem(meta):
 def case(request):
     meta, g = golden(request.param)
     F = inputs.forcing(meta["dist"], meta["n_t"], meta["n_x"])
-    asm = hw.assemble_system(_problem(meta), meta["J"], meta["K"], hw.SolveConfig(), forcing=F)
+    asm = hw.assemble_system(_problem(meta), meta["J"], meta["K"], hw.SolveConfig(), forcing=F,
+                             domain=meta.get("domain", "square"))
     P = np.random.default_rng(meta["probe_seed"]).standard_normal((meta["n_t"], meta["n_x"]))
     return meta, g, asm, P
 
 
 def test_rhs(case):
     meta, g, asm, P = case
-    assert relative_diff(asm.rhs.f_hat.array, g["fhat"]) <= 1e-13
+    # f-hat contains a K_x batch (K_Y): rounding-level on the streamed MG levels
+    tol = 1e-13 if (meta["d"] == 1 or meta["K"] <= 5) else 1e-12
+    assert relative_diff(asm.rhs.f_hat.array, g["fhat"]) <= tol
     if "g_hat" in g:
         assert relative_diff(asm.rhs.u0_part.array, g["u0_hat"]) == 0.0
-        assert relative_diff(asm.rhs.g_part.array, g["g_hat"]) <= 1e-13
+        assert relative_diff(asm.rhs.g_part.array, g["g_hat"]) <= tol
 
 
 def test_wavelet_bit_exact(case):
@@ -113,13 +119,13 @@ def test_pcg_device_resident_rtol(case):
     assert res.iterations == meta["iterations"]
 
 
-@pytest.mark.parametrize("name", ["mg8", "mg1d10"])
+@pytest.mark.parametrize("name", ["mg8", "mg1d10", "mgL8"])
 def test_multigrid_large_K(name):
     meta, g = golden(name)
-    hier = hw.build_mesh_hierarchy(meta["d"], meta["K"])
+    hier = hw.build_mesh_hierarchy(meta["d"], meta["K"], meta.get("domain", "square"))
     B = np.random.default_rng(meta["probe_seed"]).standard_normal((meta["rows"], meta["n"]))
     for s in meta["solvers"]:
-        mg = hw.make_solver(hier, s["alpha"], s["mu"])
+        mg = hw.make_solver(hier, s["alpha"], s["mu"], D=meta.get("D"))
         X = np.empty_like(B)
         mg.apply_rows(B, X, 0, B.shape[0])
         assert relative_diff(X, g[s["key"]]) <= 1e-12, s["key"]
@@ -285,3 +291,76 @@ def test_pcg_residual_recomputation_matches_oracle():
     u = asm.wavelet.apply_array(res.w.array)
     uo = ref.wavelet.apply(ro.w)
     assert np.linalg.norm(u - uo) / np.linalg.norm(uo) <= 1e-8
+
+
+def test_lshape_layout_roundtrip():
+    """hwg_grid_scatter / hwg_grid_gather: dof layout <-> embedded grid with
+    the removed quadrant zero (bit-exact, every dof once)."""
+    from paper_2009_08875_b200.device import GpuContext
+    from oracle import heatwave_oracle as O
+
+    ctx = GpuContext(2, 2, 6, D=0.25 * np.eye(2), domain="L")
+    lv = O.mesh(2, 6, "L")
+    n = 2 ** 6
+    gi = np.rint(lv.verts[lv.interior] * n).astype(int) - 1      # 0-based grid coords
+    flat = gi[:, 0] * (n - 1) + gi[:, 1]
+    X = torch.randn((3, ctx.n_x), dtype=torch.float64, device="cuda")
+    G = torch.full((3, ctx.n_grid), 7.0, dtype=torch.float64, device="cuda")
+    ctx.grid_scatter(X, G)
+    want = np.zeros((3, ctx.n_grid))
+    want[:, flat] = X.cpu().numpy()
+    assert np.array_equal(G.cpu().numpy(), want)
+    Y = torch.empty_like(X)
+    ctx.grid_gather(G, Y)
+    assert torch.equal(X, Y)
+
+
+@pytest.mark.parametrize("domain", ["square", "L"])
+def test_multigrid_K11_matches_oracle(domain):
+    """The n = 2047 register kernel (BASELINE cfg 5's finest level K = 11 on
+    the mapped L; also the square) against the oracle on seeded rows."""
+    from oracle import heatwave_oracle as O
+
+    K = 11
+    D = 0.25 * np.eye(2) if domain == "L" else None
+    k0 = 2 if domain == "L" else 1
+    levels = [O.mesh(2, k, domain) for k in range(k0, K + 1)]
+    ops = [O.assemble_p1(lv, D) for lv in levels]
+    prols = [O.prolongation(levels[k - 1], levels[k]) for k in range(1, len(levels))]
+    hier = hw.build_mesh_hierarchy(2, K, domain)
+    B = np.random.default_rng(11).standard_normal((2, hier.N_x))
+    for alpha, mu in ((1.0, 0.0), (0.3, 2.0 ** 11)):
+        want = O.Multigrid(ops, prols, alpha, mu).apply_rows(B, np.empty_like(B))
+        got = np.empty_like(B)
+        hw.make_solver(hier, alpha, mu, D=D).apply_rows(B, got, 0, 2)
+        # rounding grows with the level operator's conditioning (~4^K)
+        assert relative_diff(got, want) <= 1e-12 * 4.0 ** (K - 8), (alpha, mu)
+
+
+def test_lshape_cfg5_shaped_properties():
+    """BASELINE cfg 5's spatial size (mapped K = 11, N_x = 3,141,633) with a
+    short time axis: S-hat and K_X symmetric positive, the removed quadrant
+    never leaks into dofs (dof-layout in, dof-layout out), and a PCG solve
+    to rtol 1e-6 whose residual, recomputed, satisfies the stopping rule."""
+    prob = hw.lshape_problem()
+    J, K = 2, 11
+    n_t = 2 ** J + 1
+    F = inputs.forcing("lshape", n_t, hw.build_mesh_hierarchy(2, K, "L").N_x)
+    asm = hw.assemble_system(prob, J, K, hw.SolveConfig(), forcing=F, host_rhs=False, domain="L")
+    n_x = asm.S.n_x
+    assert n_x == 3141633
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn((n_t, n_x), dtype=torch.float64, device="cuda", generator=gen)
+    y = torch.randn((n_t, n_x), dtype=torch.float64, device="cuda", generator=gen)
+    dot = lambda a, b: float((a * b).sum())  # noqa: E731
+    Sx, Sy = asm.S.apply_array(x), asm.S.apply_array(y)
+    assert abs(dot(y, Sx) - dot(x, Sy)) <= 1e-10 * abs(dot(x, Sx))
+    Kx_, Ky_ = asm.K_X.apply_array(x), asm.K_X.apply_array(y)
+    assert abs(dot(y, Kx_) - dot(x, Ky_)) <= 1e-10 * abs(dot(x, Kx_))
+    assert dot(x, Sx) > 0 and dot(x, Kx_) > 0
+    res = hw.pcg(asm.S, asm.K_X, asm.rhs, 0.0, rtol=1e-6)
+    f = asm.rhs.f_hat.array
+    r = f - asm.S.apply_array(res.w.array)
+    rz = dot(r, asm.K_X.apply_array(r))
+    rz0 = dot(f, asm.K_X.apply_array(f))
+    assert rz <= (1.01e-6) ** 2 * rz0

@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert set(_lib.EXPORTS) == syms
     L = _lib.load()
-    assert L.hwg_version() == 3
+    assert L.hwg_version() == 4
 
 
 def test_library_is_sm100a():
@@ -168,3 +168,31 @@ def test_bench_implementation_byte_model():
     assert 85 < w4 < 95, w4
     N3 = (2 ** 20 + 1) * (2 ** 10 - 1)
     assert abs(bench.impl_bytes_per_iteration(1, 20, 10) / 8 / N3 - 35.0) < 0.01
+
+
+def test_lshape_host_setup_matches_oracle():
+    """L-shaped domain (BASELINE cfg 5, mapped): dof count, finest mesh, and
+    the level-2 dense inverses the GPU coarse kernel applies are bit-identical
+    to the oracle's (which the L1/L2/mgL8 fixtures pin to the reference)."""
+    from oracle import heatwave_oracle as O
+
+    D = 0.25 * np.eye(2)
+    for K in (2, 3, 5, 11):
+        assert disc.lshape_dofs(K) == (2 ** K - 1) ** 2 - 4 ** (K - 1)
+    assert disc.lshape_dofs(11) == 3141633          # BASELINE cfg 5: ~3.1e6 interior dofs
+    fm = disc.FineMesh(2, 5, "L")
+    lv = O.mesh(2, 5, "L")
+    assert np.array_equal(fm.interior, lv.interior)
+    assert np.array_equal(fm.elements, lv.elems)
+    system = O.assemble(2, 3, 4, D=D, domain="L")
+    ci = disc.lshape_coarse_inverses(disc.operator_list(3, 0.3), D)
+    assert np.array_equal(system.Kx._keep[-1].ravel(), ci[0])
+    for j in range(4):
+        assert np.array_equal(system.blocks[j]._keep[-1].ravel(), ci[1 + j])
+    # interior stencils of the L equal the square's with the same D
+    M, A = disc.level_stencils(2, 4, D)
+    lv4 = O.mesh(2, 4, "L")
+    Mo, Ao = O.assemble_p1(lv4, D)
+    r = int(np.nonzero(np.all(np.rint(lv4.verts[lv4.interior] * 16) == [4, 4], axis=1))[0][0])
+    assert sorted(Ao.tocsr()[r].data.tolist()) == sorted([A["c0"]] + [A["cx"]] * 2 + [A["cy"]] * 2)
+    assert inputs.CONFIGS[5]["domain"] == "L"
