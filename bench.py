@@ -19,6 +19,11 @@ GPUs (paper_2009_08875_b200/distributed.py, SURVEY §8e design (a)): NCCL
 halo rows for the temporal bands and wavelet stages, an allgather of the
 coarse wavelet levels and of the dot partials; "scaling": "strong" (total
 work fixed).  --slab runs the same distributed path at N = 1.
+
+--config 5 (L-shaped domain, N = 6.4e9 dofs, quoted "across 8 B200"): one
+GPU cannot hold it, so N GPUs run the per-GPU share of the 8-GPU problem --
+the same spatial mesh (N_x = 3,141,633, K = 11 mapped) with J = 8 + log2 N
+(N_t = 257 at N = 1; the full cfg 5, J = 11, at N = 8); "scaling": "weak".
 """
 
 from __future__ import annotations
@@ -38,6 +43,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_2009_08875_b200 import inputs  # noqa: E402
+from paper_2009_08875_b200 import discretization as disc  # noqa: E402
 
 METRIC = "space-time DoFs x PCG iters/sec (rtol 1e-6)"
 UNIT = "DoF*it/s"
@@ -62,7 +68,7 @@ def model_bytes_per_iteration(d, J, K, nu=3, cycles=2):
     return 8.0 * words
 
 
-def impl_bytes_per_iteration(d, J, K, cycles=2):
+def impl_bytes_per_iteration(d, J, K, cycles=2):  # grid layout (the L moves its zero quadrant)
     """Algorithmic HBM bytes this implementation moves per PCG iteration
     (no recomputation step): every kernel's compulsory reads + writes, 8 B
     words.  DESIGN.md §5 lists the terms; ncu confirms DRAM traffic = these
@@ -162,10 +168,30 @@ def dist_env():
     return rank, world, local
 
 
-def workload(cfg):
+def workload(cfg, world=1):
     d, J, K, dist, u0 = inputs.recipe(cfg)
-    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** d
+    if cfg == 5:                       # per-GPU share of the 8-GPU problem (weak scaling)
+        J = 8 + (world.bit_length() - 1)
+    n_t = 2 ** J + 1
+    n_x = disc.lshape_dofs(K) if domain_of(cfg) == "L" else (2 ** K - 1) ** d
     return d, J, K, dist, u0, n_t, n_x
+
+
+def domain_of(cfg):
+    return inputs.CONFIGS[cfg].get("domain", "square")
+
+
+def diffusion_of(cfg, d):
+    """D of the config (the L is mapped to [0,1]^2 minus [1/2,1]^2: D = I/4)."""
+    return 0.25 * np.eye(2) if domain_of(cfg) == "L" else np.eye(d)
+
+
+def workload_label(cfg, d, J, K, n_t, n_x, world=1):
+    if cfg == 5:
+        return (f"cfg5: 2D L-shaped heat (mapped, D=I/4), J={J} (N_t={n_t}), K={K} "
+                f"(N_x={n_x}), PCG to rtol 1e-6 -- the per-GPU share of cfg 5 on 8 GPUs "
+                f"(full cfg 5 is J=11 at N=8)")
+    return (f"cfg{cfg}: {d}D heat, J={J} (N_t={n_t}), K={K} (N_x={n_x}), PCG to rtol 1e-6")
 
 
 # --------------------------------------------------------------------------
@@ -179,7 +205,7 @@ def oracle_setup(cfg, fhat=None, max_dofs=4.5e7):
     Jo = J
     while (2 ** Jo + 1) * n_x > max_dofs and Jo > 2:
         Jo -= 1
-    system = O.assemble(d, Jo, K)
+    system = O.assemble(d, Jo, K, D=diffusion_of(cfg, d), domain=domain_of(cfg))
     nto = 2 ** Jo + 1
     if fhat is not None and Jo == J:
         f = np.ascontiguousarray(fhat)
@@ -253,10 +279,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     d, J, K, dist_name, u0, n_t, n_x = workload(args.config)
     N = n_t * n_x
-    problem = hw.ProblemData(D=np.eye(d), c=0.0, u0=u0)
+    problem = hw.ProblemData(D=diffusion_of(args.config, d), c=0.0, u0=u0)
     F = inputs.forcing(dist_name, n_t, n_x)
     asm = hw.assemble_system(problem, J, K, hw.SolveConfig(device=local), forcing=F,
-                             host_rhs=False)
+                             host_rhs=False, domain=domain_of(args.config))
     del F
     ctx = asm.ctx
     f = asm.rhs.f_hat.array
@@ -354,10 +380,11 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE recipe: F~U[-1,1] nodal forcing, u0=sin sin)",
-            "config": {"workload": f"cfg{args.config}: {d}D heat, J={J} (N_t={n_t}), "
-                                   f"K={K} (N_x={n_x}), PCG to rtol 1e-6",
+            "higher_is_better": True, "scaling": "weak" if args.config == 5 else "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded BASELINE cfg{args.config} recipe: {dist_name} nodal "
+                    "forcing, blockwise-seeded)",
+            "config": {"workload": workload_label(args.config, d, J, K, n_t, n_x),
                        "dofs": N, "iterations_per_solve": its_list[0],
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (each solve streams >100 arrays of "
@@ -406,9 +433,11 @@ def run_slab(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     tdist.init_process_group("nccl", device_id=dev)
-    d, J, K, dist_name, u0, n_t, n_x = workload(args.config)
+    d, J, K, dist_name, u0, n_t, n_x = workload(args.config, world)
     N = n_t * n_x
-    states = D.make_states(d, J, K, world, [rank], lambda p: dev)
+    domain = domain_of(args.config)
+    states = D.make_states(d, J, K, world, [rank], lambda p: dev, D=diffusion_of(args.config, d),
+                           domain=domain)
     system = D.SlabSystem(states, D.TorchComm())
     st = states[0]
     lay = st.lay
@@ -416,7 +445,7 @@ def run_slab(args):
     def frows(a, b):
         return torch.from_numpy(inputs.forcing_rows(dist_name, n_t, n_x, a, b)).to(dev)
 
-    u0p = torch.from_numpy(disc.project_initial(disc.FineMesh(d, K), u0)).to(dev)
+    u0p = torch.from_numpy(disc.project_initial(disc.FineMesh(d, K, domain), u0)).to(dev)
     F = D.rhs(system, frows, u0p)
     W = [torch.empty_like(F[0])]
 
@@ -449,8 +478,9 @@ def run_slab(args):
     value = N * total_its / (ms_max / 1e3)
 
     # e2e: pinned host f-hat rows in, u rows out, every step
-    fh = [torch.empty(F[0].shape, dtype=torch.float64, pin_memory=True)]
-    fh[0].copy_(F[0])
+    Fd = D.from_grid(st, F[0])                       # the user-facing (dof-layout) f-hat rows
+    fh = [torch.empty(Fd.shape, dtype=torch.float64, pin_memory=True)]
+    fh[0].copy_(Fd)
     uh = [torch.empty((lay.n_out, n_x), dtype=torch.float64, pin_memory=True)]
     D.solve_host(system, fh, uh)
     tdist.barrier()
@@ -474,10 +504,10 @@ def run_slab(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if args.config == 5 else "strong",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE recipe, blockwise-seeded forcing rows)",
-            "config": {"workload": f"cfg{args.config}: {d}D heat, J={J} (N_t={n_t}), "
-                                   f"K={K} (N_x={n_x}), PCG to rtol 1e-6",
+            "config": {"workload": workload_label(args.config, d, J, K, n_t, n_x, world),
                        "dofs": N, "iterations_per_solve": its_list[0],
                        "parallelism": f"time slabs x{world} (NCCL halos + allgather)",
                        "l2": "inputs larger than L2"},
@@ -515,7 +545,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=4, choices=(1, 2, 3, 4))
+    ap.add_argument("--config", type=int, default=4, choices=(1, 2, 3, 4, 5))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-iterations", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -21,6 +21,12 @@ with the reference's fixed pairwise tree on every rank, so inner products
 reference's worker-count determinism (tests/test_solver.py:129-142).  K_X
 and every multigrid solve are row-local: no communication.
 
+L-shaped domain (BASELINE cfg 5): every slab array is in the embedded grid
+layout of the kernel contexts (removed quadrant held at zero); the
+user-facing inputs and outputs (forcing rows, u0 moments, host f-hat / u in
+``solve_host``) are in the dof layout and converted by hwg_grid_scatter /
+hwg_grid_gather on the rank that owns them.
+
 The code is SPMD over a list of rank states.  A real run holds its own
 state and a ``TorchComm`` (NCCL between GPUs, gloo on CPUs); ``SimComm``
 holds all P states in one process and delivers messages by copying, which
@@ -442,10 +448,15 @@ class CudaKernels:
     """Local kernels of one rank: a kernel-only hwg context on its GPU."""
 
     def __init__(self, d, J, K, alpha=0.3, vcycles=2, smooth=3, device=0, rows_max=0, D=None,
-                 c=0.0):
+                 c=0.0, domain="square"):
         from .device import GpuContext
-        self.ctx = GpuContext(d, J, K, alpha, vcycles, smooth, D, c, device, rows_max=rows_max)
+        self.ctx = GpuContext(d, J, K, alpha, vcycles, smooth, D, c, device, rows_max=rows_max,
+                              domain=domain)
         ctx = self.ctx
+        self.domain = domain
+        self.n_dof = ctx.n_x
+        self.grid_scatter = ctx.grid_scatter
+        self.grid_gather = ctx.grid_gather
         self.syn_stage = ctx.syn_stage
         self.ana_stage = ctx.ana_stage
         self.bside_rows = ctx.bside_rows
@@ -460,8 +471,10 @@ class CudaKernels:
         self.temporal_rows = ctx.temporal_rows
 
 
-def make_states(d, J, K, P, ranks, device_of, alpha=0.3, vcycles=2, smooth=3):
-    """RankStates (CUDA kernels) for the given ranks of a P-rank slab run."""
+def make_states(d, J, K, P, ranks, device_of, alpha=0.3, vcycles=2, smooth=3, D=None, c=0.0,
+                domain="square"):
+    """RankStates (CUDA kernels) for the given ranks of a P-rank slab run
+    (arrays in the kernels' grid layout: (2^K - 1)^d points per row)."""
     import torch
     states = []
     n_x = (2 ** K - 1) ** d
@@ -469,9 +482,34 @@ def make_states(d, J, K, P, ranks, device_of, alpha=0.3, vcycles=2, smooth=3):
         lay = slab_layout(J, P, p)
         dev = device_of(p)
         rows_max = max(2 * lay.n_out, lay.n_w, 2 ** J // P + 2) + 2
-        kern = CudaKernels(d, J, K, alpha, vcycles, smooth, dev.index or 0, rows_max=rows_max)
+        kern = CudaKernels(d, J, K, alpha, vcycles, smooth, dev.index or 0, rows_max=rows_max,
+                           D=D, c=c, domain=domain)
         states.append(RankState(lay, kern, n_x, dev, torch.float64))
     return states
+
+
+def _is_lshape(st):
+    return getattr(st.k, "domain", "square") == "L"
+
+
+def to_grid(st, X):
+    """dof-layout rows -> the rank's grid layout (identity on the square)."""
+    import torch
+    if not _is_lshape(st):
+        return X
+    Y = torch.empty((X.shape[0], st.mid.shape[1]), dtype=X.dtype, device=X.device)
+    st.k.grid_scatter(X.contiguous(), Y)
+    return Y
+
+
+def from_grid(st, X):
+    """grid-layout rows -> dof layout (identity on the square)."""
+    import torch
+    if not _is_lshape(st):
+        return X
+    Y = torch.empty((X.shape[0], st.k.n_dof), dtype=X.dtype, device=X.device)
+    st.k.grid_gather(X.contiguous(), Y)
+    return Y
 
 
 def scatter_wavelet(X, lay: RankLayout):
@@ -502,7 +540,8 @@ def rhs(system: SlabSystem, forcing_rows, u0proj):
 
     forcing_rows(r0, r1) -> nodal forcing rows [r0, r1) as a tensor on the
     rank's device (the blockwise-seeded generator makes them independent of
-    P); u0proj: the N_x moments <u0, phi_i> (used by rank 0 only).  Returns
+    P); u0proj: the N_x moments <u0, phi_i> (used by rank 0 only); both in
+    the dof layout.  Returns
     one wavelet-local array per state.  Each rank assembles the test-space
     load of the time elements touching its slab (one halo element), applies
     K_Y = O^-1 (x) K_x (O = I) row-locally, B^T on its nodal rows and the
@@ -515,7 +554,7 @@ def rhs(system: SlabSystem, forcing_rows, u0proj):
         lay = st.lay
         H = lay.H
         e0, e1 = max(lay.p * H - 1, 0), min(lay.p * H + H, nt - 1)     # time elements
-        Fr = forcing_rows(e0, e1 + 1)                                   # nodes e0..e1
+        Fr = to_grid(st, forcing_rows(e0, e1 + 1))                     # nodes e0..e1
         MxF = torch.empty_like(Fr)
         st.k.spatial(0, Fr, MxF)
         y = torch.empty((2 * (e1 - e0), Fr.shape[1]), dtype=Fr.dtype, device=Fr.device)
@@ -535,7 +574,7 @@ def rhs(system: SlabSystem, forcing_rows, u0proj):
         xa = st.bufs["Xa"]
         xa.zero_()
         if st.lay.p == 0 and u0proj is not None:
-            xa[1].copy_(u0proj)
+            xa[1].copy_(to_grid(st, u0proj.reshape(1, -1))[0])
         U.append(torch.empty_like(G[len(U)]))
     system.analysis(U)
     return [g + u for g, u in zip(G, U)]
@@ -545,13 +584,14 @@ def solve_host(system: SlabSystem, f_host, u_host, rtol=1e-6, epsilon=0.0, max_i
     """End-to-end slab solve with host buffers (bench e2e leg): copies this
     rank's f-hat rows in, runs PCG, forms its nodal rows of u = W w and
     copies them out.  f_host / u_host: lists of pinned host tensors per
-    state ((n_w, N_x) and (n_out, N_x))."""
+    state ((n_w, N_x) and (n_out, N_x), dof layout)."""
     import torch
-    F = [fh.to(st.bufs["U"].device, non_blocking=True) for fh, st in zip(f_host, system.states)]
+    F = [to_grid(st, fh.to(st.bufs["U"].device, non_blocking=True))
+         for fh, st in zip(f_host, system.states)]
     W = [torch.empty_like(f) for f in F]
     res = pcg(system, F, W, epsilon=epsilon, rtol=rtol, max_iterations=max_iterations)
     system.synthesis(W)
     for st, uh in zip(system.states, u_host):
-        uh.copy_(st.bufs["U"][1:1 + st.lay.n_out], non_blocking=True)
+        uh.copy_(from_grid(st, st.bufs["U"][1:1 + st.lay.n_out]), non_blocking=True)
     torch.cuda.synchronize()
     return res

@@ -41,11 +41,14 @@ def test_layout_rejects_bad_P():
         D.slab_layout(3, 8, 0)
 
 
-def _oracle_case(d, J, K, dist="uniform"):
+def _oracle_case(d, J, K, dist="uniform", domain="square"):
     from oracle import heatwave_oracle as O
-    system = O.assemble(d, J, K)
+    if domain == "L":
+        system = O.assemble(d, J, K, D=0.25 * np.eye(2), domain="L")
+    else:
+        system = O.assemble(d, J, K)
     n_t, n_x = system.shape
-    u0 = inputs.u0_sines if dist == "uniform" else inputs.u0_modes()
+    u0 = inputs.u0_sines if dist in ("uniform", "lshape") else inputs.u0_modes()
     f = system.rhs(inputs.forcing(dist, n_t, n_x), u0)
     eps = 1e-6 * np.sqrt(O.dot(f, system.kx(f)))
     ref = O.pcg(system, f, eps)
@@ -77,6 +80,17 @@ def test_simulated_ranks_match_oracle_bitwise(d, J, K, P):
     # replicated coarse rows are identical on every rank
     for st, x in zip(states, W):
         assert np.array_equal(x[:P + 1].numpy(), ref.w[:P + 1])
+
+
+@pytest.mark.parametrize("J,K,P", [(3, 4, 2), (4, 5, 4)])
+def test_simulated_ranks_lshape_match_oracle_bitwise(J, K, P):
+    """The L-shaped domain (BASELINE cfg 5) over time slabs: bit-identical
+    to the oracle's single-process PCG."""
+    O, system, f, eps, ref = _oracle_case(2, J, K, "lshape", domain="L")
+    states, W, res = _run_slabs(system, f, eps, P, D.SimComm(P), range(P))
+    assert res.iterations == ref.iterations
+    w = D.gather_wavelet([x.numpy() for x in W], [st.lay for st in states], np.zeros_like(f))
+    assert np.array_equal(w, ref.w)
 
 
 def _free_port():
@@ -182,3 +196,41 @@ def test_gpu_virtual_ranks_rhs(d, J, K, P):
     parts = D.rhs(D.SlabSystem(states, D.SimComm(P)), lambda a, b: Ft[a:b], u0p)
     got = D.gather_wavelet(parts, [st.lay for st in states], torch.zeros_like(asm.rhs.f_hat.array))
     assert torch.equal(got, asm.rhs.f_hat.array)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("J,K,Ps", [(3, 5, (2, 4)), (4, 7, (1, 4)), (4, 11, (2,))])
+def test_gpu_virtual_ranks_lshape(J, K, Ps):
+    """L-shaped domain: P virtual ranks (grid layout, dof-layout RHS inputs)
+    reproduce the single-GPU solve bit for bit -- f-hat and w."""
+    import paper_2009_08875_b200 as hw
+    from paper_2009_08875_b200 import discretization as disc
+    prob = hw.lshape_problem(u0=inputs.u0_sines)
+    n_t = 2 ** J + 1
+    n_x = disc.lshape_dofs(K)
+    F = inputs.forcing("lshape", n_t, n_x)
+    asm = hw.assemble_system(prob, J, K, hw.SolveConfig(), forcing=F, host_rhs=False, domain="L")
+    ctx = asm.ctx
+    f = asm.rhs.f_hat.array
+    w1 = torch.empty_like(f)
+    stats, rc = ctx.pcg(f, w1, 0.0, 1e-6)
+    assert rc == 0
+    fg = torch.empty((n_t, ctx.n_grid), dtype=torch.float64, device="cuda")
+    ctx.grid_scatter(f, fg)
+    dev = torch.device("cuda", 0)
+    u0p = torch.from_numpy(disc.project_initial(disc.FineMesh(2, K, "L"), prob.u0)).to(dev)
+    Ft = torch.from_numpy(F).to(dev)
+    for P in Ps:
+        states = D.make_states(2, J, K, P, range(P), lambda p: dev, D=0.25 * np.eye(2),
+                               domain="L")
+        system = D.SlabSystem(states, D.SimComm(P))
+        parts = D.rhs(system, lambda a, b: Ft[a:b], u0p)
+        got = D.gather_wavelet(parts, [st.lay for st in states], torch.zeros_like(fg))
+        assert torch.equal(got, fg), P
+        Wl = [torch.zeros_like(x) for x in parts]
+        res = D.pcg(system, parts, Wl, rtol=1e-6)
+        assert res.iterations == stats["iterations"], P
+        wg = D.gather_wavelet(Wl, [st.lay for st in states], torch.zeros_like(fg))
+        w = torch.empty_like(w1)
+        ctx.grid_gather(wg, w)
+        assert torch.equal(w, w1), (P, float((w - w1).abs().max()))
