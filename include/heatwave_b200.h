@@ -141,6 +141,12 @@ int hwg_spatial(hwg_ctx *ctx, int which, const double *X, double *Y, int64_t row
 /* SchurOperator.apply_array, five-term form (system.py:116-147, 182-187). */
 int hwg_schur_apply(hwg_ctx *ctx, const double *X, double *Y, void *stream);
 
+/* SchurOperator form (system.py:84-87, SolveConfig.form): 0 = "five_term"
+ * (Lemma 2, the production path, default), 1 = "test_space" (Lemma 1:
+ * B^T K_Y B + Gamma0 through the test-space matrices, system.py:149-180).
+ * hwg_schur_apply and hwg_pcg apply the selected form. */
+int hwg_set_schur_form(hwg_ctx *ctx, int form);
+
 /* PreconditionerKX.apply_array (system.py:252-276). */
 int hwg_kx_apply(hwg_ctx *ctx, const double *X, double *Y, void *stream);
 

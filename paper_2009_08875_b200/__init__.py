@@ -13,7 +13,7 @@ from .api import (SolveConfig, SpaceTimeVector, TemporalDiscretization, MeshHier
                   build_mesh_hierarchy, WaveletTransform, MultigridSolver, make_solver,
                   SchurOperator, PreconditionerKX, RightHandSide, ProblemAssembly,
                   assemble_system, assemble_rhs, PCGResult, pcg, solve_heat, HeatSolution,
-                  measure_error, estimate_condition, lanczos_tridiagonal, ParallelPlan,
+                  measure_error, estimate_condition, lanczos_tridiagonal, lanczos_condition, ParallelPlan,
                   split_ranges, tree_reduce, project_initial, decaying_heat, forced_heat,
                   PROBLEMS)
 

@@ -25,7 +25,7 @@ EXPORTS = ("hwg_last_error", "hwg_version", "hwg_create", "hwg_destroy",
            "hwg_kx_apply", "hwg_mg_rows", "hwg_rhs", "hwg_dot", "hwg_pcg",
            "hwg_solve_host", "hwg_launch_count", "hwg_profile_enable", "hwg_profile_read",
            "hwg_syn_stage", "hwg_ana_stage", "hwg_bside_rows", "hwg_bt_rows", "hwg_mg_rows_dev",
-           "hwg_mg_rows_dev_dot", "hwg_grid_scatter", "hwg_grid_gather",
+           "hwg_mg_rows_dev_dot", "hwg_grid_scatter", "hwg_grid_gather", "hwg_set_schur_form",
            "hwg_row_partials", "hwg_tree_sum", "hwg_axpy", "hwg_xpay", "hwg_temporal_rows")
 
 _P = C.c_void_p
@@ -97,6 +97,7 @@ def load(build_if_missing=True):
     L.hwg_mg_rows_dev.argtypes = [_P, _P, _P, _P, _I64, _P]
     L.hwg_mg_rows_dev_dot.argtypes = [_P, _P, _P, _P, _I64, _P, _P, _P]
     L.hwg_grid_scatter.argtypes = [_P, _P, _P, _I64, _P]
+    L.hwg_set_schur_form.argtypes = [_P, C.c_int]
     L.hwg_grid_gather.argtypes = [_P, _P, _P, _I64, _P]
     L.hwg_row_partials.argtypes = [_P, _P, _P, _I64, _P, _P]
     L.hwg_tree_sum.argtypes = [_P, _P, _I64, _P, _P]

@@ -29,6 +29,7 @@ __all__ = [
     "SchurOperator", "PreconditionerKX", "RightHandSide", "ProblemAssembly",
     "assemble_system", "PCGResult", "IterationLimitError", "pcg", "solve_heat",
     "HeatSolution", "measure_error", "estimate_condition", "lanczos_tridiagonal",
+    "lanczos_condition",
     "ParallelPlan", "split_ranges", "tree_reduce", "ProblemData", "project_initial",
     "decaying_heat", "forced_heat", "PROBLEMS",
 ]
@@ -299,10 +300,9 @@ class SchurOperator:
     def __init__(self, ctx: GpuContext, form="five_term"):
         if form not in ("test_space", "five_term"):
             raise ValueError("form must be 'five_term' or 'test_space'")
-        if form == "test_space":
-            raise NotImplementedError("the GPU path implements the production five-term form")
         self.ctx = ctx
         self.form = form
+        ctx.set_schur_form(form)          # also the form pcg applies (SolveConfig.form)
 
     @property
     def n_t(self):
@@ -316,6 +316,7 @@ class SchurOperator:
         torch = _torch()
         x, host = _in(self.ctx, X, (self.n_t, self.n_x))
         y = torch.empty_like(x)
+        self.ctx.set_schur_form(self.form)
         self.ctx.schur(x, y)
         return _out(self.ctx, y, host, out)
 
@@ -542,6 +543,7 @@ def pcg(S: SchurOperator, K: PreconditionerKX, f_hat, epsilon: float,
     fv = f_hat.f_hat if isinstance(f_hat, RightHandSide) else f_hat
     f, host = _in(ctx, fv.array, (ctx.n_t, ctx.n_x))
     w = torch.empty_like(f)
+    ctx.set_schur_form(S.form)
     t0 = time.perf_counter()
     stats, rc = ctx.pcg(f, w, epsilon, rtol, max_iterations, recompute_every)
     times = {"schur": stats["ms_schur"] / 1e3, "precond": stats["ms_precond"] / 1e3,
@@ -552,6 +554,52 @@ def pcg(S: SchurOperator, K: PreconditionerKX, f_hat, epsilon: float,
     wv = SpaceTimeVector(w.cpu().numpy() if host else w)
     return PCGResult(wv, k, stats["residual_norms"], kappa, times, stats["alphas"],
                      stats["betas"])
+
+
+def lanczos_condition(S: SchurOperator, K: PreconditionerKX, seed: int = 0,
+                      tol: float = 1e-4, max_iterations: int = 250, check_every: int = 10):
+    """Converged kappa_2(K_X S-hat) from a random-vector CG-Lanczos run
+    (solver.py:266-300): iterate until the extreme Ritz values settle.
+
+    The CG recurrences run on the device (the C ABI's operators, dots and
+    axpys); only the scalars come back.  Dots use the reference's per-row
+    partials + fixed tree (the reference here sums with numpy), so kappa
+    agrees to rounding, the stopping iteration exactly unless a check lands
+    within rounding of ``tol``."""
+    torch = _torch()
+    if S.ctx is not K.ctx:
+        raise ValueError("S and K_X must come from the same assembled system")
+    ctx = S.ctx
+    rng = np.random.default_rng(seed)
+    f = torch.from_numpy(rng.standard_normal((S.n_t, S.n_x))).to(ctx.device)
+    r = f.clone()
+    z = K.apply_array(r)
+    rho = ctx.dot(r, z)
+    p = z.clone()
+    alphas, betas = [], []
+    prev = None
+    for k in range(1, max_iterations + 1):
+        q = S.apply_array(p)
+        pq = ctx.dot(p, q)
+        if pq <= 0:
+            break
+        alpha = rho / pq
+        ctx.axpy(-alpha, q, r)
+        z = K.apply_array(r)
+        rho_new = ctx.dot(r, z)
+        if rho_new <= 0:
+            break
+        beta = rho_new / rho
+        alphas.append(alpha)
+        betas.append(beta)
+        rho = rho_new
+        ctx.xpay(beta, z, p)                 # p = z + beta p
+        if k >= check_every and k % check_every == 0:
+            kap = _kappa_from_cg(alphas, betas)
+            if prev is not None and abs(kap - prev) <= tol * kap:
+                return kap, k
+            prev = kap
+    return _kappa_from_cg(alphas, betas), len(alphas)
 
 
 @dataclass

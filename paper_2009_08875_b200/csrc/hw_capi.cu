@@ -58,6 +58,7 @@ struct hwg_ctx {
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
+    int form = 0;                      // S: 0 five-term (Lemma 2), 1 test-space (Lemma 1)
     int64_t nxu = 0, Nu = 0;           // dof-layout row length / size (= nx, N for domain 0)
     double *cinv = nullptr;            // domain 1: [op][25] level-2 inverses (device)
     double *Xg = nullptr, *Yg = nullptr;   // domain 1: grid-layout operands of full contexts
@@ -389,9 +390,33 @@ static int wavelet(hwg_ctx *c, const double *X, double *Y, double *S1, double *S
     return HWG_OK;
 }
 
+// test-space S-hat = W^T (B^T K_Y B + Gamma0) W (system.py:149-180, Lemma 1):
+// y = T (M_x U) + N (A_x U) on the 2 2^J test rows, K_Y = O^-1 (x) K_x with
+// O = I (temporal.py:141; dividing by 1.0 is exact), then B^T = T^T (x) M_x +
+// N^T (x) A_x and the trace row -- the cross-check of the production five-term
+// form, in the reference's operation order
+static int schur_test_space(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
+{
+    const int64_t nt = c->nt, nx = c->nx, N = c->N, ntest = 2 * (nt - 1);
+    TRY(wavelet(c, X, c->U, c->T12, c->T12 + N, false, st));
+    CK(launch_stencil_rows(c->U, c->MxU, c->AxU, c->grid, c->SM, c->SA, nt, st));
+    BandOut y{c->T.view(), c->Nn.view(), c->MxU, c->AxU, c->T12};
+    CK(launch_temporal_bands(y, BandOut{}, ntest, nx, st));
+    c->launches += 2;
+    TRY(mg_apply(c, c->T12, c->G12, ntest, 0, nullptr, st));
+    BandOut w1{c->TT.view(), TCsr{nullptr, nullptr, nullptr}, c->G12, nullptr, c->U};
+    BandOut w2{c->NT.view(), TCsr{nullptr, nullptr, nullptr}, c->G12, nullptr, c->AxU};
+    CK(launch_temporal_bands(w1, w2, nt, nx, st));
+    CK(launch_bt_side(c->U, c->AxU, c->MxU, c->G12, c->grid, c->SM, c->SA, nt, st));
+    c->launches += 2;
+    TRY(wavelet(c, c->G12, Y, c->T12, c->T12 + N, true, st));
+    return HWG_OK;
+}
+
 // five-term S-hat = W^T S W (system.py:116-147, 182-187)
 static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
 {
+    if (c->form == 1) return schur_test_space(c, X, Y, st);
     const int64_t nt = c->nt, N = c->N;
     TRY(wavelet(c, X, c->U, c->T12, c->T12 + N, false, st));
     // t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU (one pass over U); the
@@ -665,6 +690,13 @@ int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
     TRY(to_grid(c, X, c->Xg, c->nt, S(stream)));
     TRY(kx(c, c->Xg, c->Yg, S(stream)));
     return from_grid(c, c->Yg, Y, c->nt, S(stream));
+}
+
+int hwg_set_schur_form(hwg_ctx *c, int form)
+{
+    if (!c || (form != 0 && form != 1)) return fail(HWG_EINVAL, "form must be 0 (five-term) or 1 (test-space)");
+    c->form = form;
+    return HWG_OK;
 }
 
 int hwg_grid_scatter(hwg_ctx *c, const double *X, double *Y, int64_t rows, void *stream)

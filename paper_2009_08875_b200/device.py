@@ -149,6 +149,10 @@ class GpuContext:
         _lib.check(self.lib.hwg_temporal_rows(self.handle, self.BANDS[band], ptr(X), x0, ptr(Y),
                                               r0, nr, self.stream()))
 
+    def set_schur_form(self, form):
+        """"five_term" (default) or "test_space" for schur() and pcg()."""
+        _lib.check(self.lib.hwg_set_schur_form(self.handle, {"five_term": 0, "test_space": 1}[form]))
+
     def grid_scatter(self, X, Y):
         """dof-layout rows X -> grid-layout rows Y (L-shaped domain)."""
         _lib.check(self.lib.hwg_grid_scatter(self.handle, ptr(X), ptr(Y), X.shape[0], self.stream()))

@@ -241,6 +241,27 @@ def wavelet_case(name, J, cols):
     print(f"{name}: done", flush=True)
 
 
+def test_space_case(name, d, J, K, dist, domain="square", D=None):
+    """The reference's Lemma-1 (test-space) Schur form on a probe, the
+    five-term form on the same probe, and its Lanczos condition estimate
+    (solver.py:266-300) with default arguments."""
+    problem = problem_for(d, dist, D)
+    asm = assemble_reference(problem, J, K, domain)
+    n_t, n_x = asm.S.n_t, asm.S.n_x
+    St = hw.SchurOperator(temporal=asm.temporal, spatial=asm.spatial, K_x=asm.K_x,
+                          wavelet=asm.wavelet, form="test_space", test=asm.test)
+    P = np.random.default_rng(PROBE_SEED).standard_normal((n_t, n_x))
+    kappa, k = hw.lanczos_condition(asm.S, asm.K_X)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), STP=St.apply_array(P),
+                        SP=asm.S.apply_array(P))
+    meta = dict(name=name, d=d, J=J, K=K, dist=dist, n_t=n_t, n_x=n_x, domain=domain,
+                D=np.asarray(problem.D, dtype=float).tolist(), probe_seed=PROBE_SEED,
+                lanczos_kappa=float(kappa), lanczos_iterations=int(k))
+    with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(f"{name}: lanczos kappa={kappa} k={k}", flush=True)
+
+
 def check_interpolant_load():
     """(N (x) M_x) F == assemble_load of the P1 x P1 interpolant of F."""
     for d, J, K in ((1, 3, 4), (2, 2, 3)):
@@ -302,6 +323,8 @@ CASES = {
                            u0=inputs.u0_sines),
     "L2": lambda: run_case("L2", 2, 4, 7, "lshape", lean=True, D=0.25 * np.eye(2), domain="L"),
     "mgL8": lambda: mg_rows_case("mgL8", 2, 8, rows=2, domain="L", D=0.25 * np.eye(2)),
+    "ts1": lambda: test_space_case("ts1", 2, 4, 4, "uniform"),
+    "ts2": lambda: test_space_case("ts2", 2, 3, 7, "lshape", domain="L", D=0.25 * np.eye(2)),
     "d2": lambda: run_case("d2", 1, 10, 10, "normal", full=False),
     "cfg2": lambda: run_case("cfg2", 2, 8, 8, "uniform", full=False),
     "mg8": lambda: mg_rows_case("mg8", 2, 8),

@@ -364,3 +364,32 @@ def test_lshape_cfg5_shaped_properties():
     rz = dot(r, asm.K_X.apply_array(r))
     rz0 = dot(f, asm.K_X.apply_array(f))
     assert rz <= (1.01e-6) ** 2 * rz0
+
+
+@pytest.mark.parametrize("name", ["ts1", "ts2"])
+def test_test_space_form_and_lanczos(name):
+    """SolveConfig.form = "test_space" (Lemma 1, system.py:149-180) against
+    the reference's own test-space apply; five-term == test-space to 1e-12
+    (test_system.py:60-71); lanczos_condition (solver.py:266-300) against
+    the reference's converged kappa and stopping iteration."""
+    meta, g = golden(name)
+    domain = meta.get("domain", "square")
+    prob = hw.ProblemData(D=np.asarray(meta["D"]), c=0.0, u0=inputs.u0_for(meta["dist"]))
+    asm = hw.assemble_system(prob, meta["J"], meta["K"], hw.SolveConfig(form="test_space"),
+                             domain=domain)
+    P = np.random.default_rng(meta["probe_seed"]).standard_normal((meta["n_t"], meta["n_x"]))
+    st = asm.S.apply_array(P)
+    tol = 0.0 if meta["K"] <= 5 else 1e-12
+    assert relative_diff(st, g["STP"]) <= tol
+    five = hw.SchurOperator(asm.ctx, "five_term")
+    assert relative_diff(five.apply_array(P), g["SP"]) <= max(tol, 1e-13)
+    assert relative_diff(five.apply_array(P), st) <= 1e-12
+    kappa, k = hw.lanczos_condition(five, asm.K_X)
+    assert k == meta["lanczos_iterations"]
+    assert abs(kappa - meta["lanczos_kappa"]) <= 1e-8 * meta["lanczos_kappa"]
+    # a test-space PCG solve reaches the same iterate as the five-term one
+    r_ts = hw.pcg(asm.S, asm.K_X, asm.rhs, 0.0, rtol=1e-6)
+    r_5 = hw.pcg(five, asm.K_X, asm.rhs, 0.0, rtol=1e-6)
+    assert r_ts.iterations == r_5.iterations
+    w5 = r_5.w.array
+    assert np.linalg.norm(r_ts.w.array - w5) <= 1e-10 * np.linalg.norm(w5)
