@@ -18,11 +18,15 @@ ap.add_argument("--K", type=int, default=8)
 ap.add_argument("--d", type=int, default=2)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--what", default="mg")
+ap.add_argument("--domain", default="square", choices=("square", "L"))
 a = ap.parse_args()
-asm = hw.assemble_system(hw.decaying_heat(a.d), a.J, a.K, hw.SolveConfig(), host_rhs=False)
+prob = hw.lshape_problem() if a.domain == "L" else hw.decaying_heat(a.d)
+asm = hw.assemble_system(prob, a.J, a.K, hw.SolveConfig(), host_rhs=False, domain=a.domain)
 ctx = asm.ctx
 n_t, n_x = ctx.n_t, ctx.n_x
 x = torch.randn((2 * n_t, n_x), dtype=torch.float64, device="cuda")
+if a.domain == "L":        # MG rows in the dof layout (the entry point scatters to the grid)
+    pass
 y = torch.empty_like(x)
 for _ in range(a.reps):
     if a.what == "mg":
