@@ -57,6 +57,7 @@ struct hwg_ctx {
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
     int64_t small_rows = 0;             // see MgStreamArgs::small_rows
+    int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
     int form = 0;                      // S: 0 five-term (Lemma 2), 1 test-space (Lemma 1)
@@ -310,7 +311,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
         }
         if (c->K <= kCoarseTop2d) {
             MgCoarseArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, 1, ro, op, nr,
-                           c->domain, c->cinv};
+                           c->domain, c->cinv, 0};
             ProfScope ps(c, st, 4, 16.0 * nr * c->nx);
             CK(mg2d_coarse_launch(a, st));
             ++c->launches;
@@ -343,7 +344,8 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
             }
             MgCoarseArgs ca{c->mgB[kCoarseTop2d], level_size(c, kCoarseTop2d),
                             c->mgX[kCoarseTop2d], level_size(c, kCoarseTop2d), c->coef,
-                            c->K + 1, kCoarseTop2d, 1, 1, ro, op, nr, c->domain, c->cinv};
+                            c->K + 1, kCoarseTop2d, 1, 1, ro, op, nr, c->domain, c->cinv,
+                            c->coarse_fast};
             {
                 ProfScope ps(c, st, 4, 16.0 * nr * level_size(c, kCoarseTop2d));
                 CK(mg2d_coarse_launch(ca, st));
@@ -541,6 +543,8 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         else if (ev[0] == '4' && c->mg_reg_ok) c->mg_reg_ok = 2;   // P = 4 at n = 1023
         else if (ev[0] == '5' && c->mg_reg_ok) c->mg_reg_ok = 3;   // P = 4 for UP at n = 1023
     if (const char *ev = getenv("HWG_REG_SMALL_ROWS")) c->small_rows = atoll(ev);
+    if (const char *ev = getenv("HWG_COARSE_EXACT"))        // A/B switch for measurements
+        if (ev[0] == '1') c->coarse_fast = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask
     if (!c->mg_reg_ok && d.dim == 2 && d.K > kCoarseTop2d && (d.K > 10 || d.domain)) {
         delete c;

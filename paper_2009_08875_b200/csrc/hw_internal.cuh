@@ -41,6 +41,8 @@ struct MgCoarseArgs {
     int64_t rows;
     int lshape;              // mapped L-shaped domain: masked quadrant, level-2 dense solve
     const double *cinv;      // lshape: [op][25] inverse of the 5-dof level-2 operator
+    int fast;                // below streamed levels: multiply by 1/c0, tree sums (not
+                             // bit-exact); 0 = the reference's CSR-order arithmetic
 };
 
 constexpr int kCoarseTop2d = 5;

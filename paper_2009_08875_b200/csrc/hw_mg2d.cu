@@ -427,9 +427,10 @@ constexpr int kCoarseWords = 2 * kCoarseStack + Lc<kCoarseTop2d>::size;   // x, 
 
 // level coefficients in registers
 struct Cf {
-    double c0, cx, cy, cd;
+    double c0, cx, cy, cd, inv;
     bool diag;
-    HW_DEV Cf(const double *c) : c0(c[kC0]), cx(c[kCx]), cy(c[kCy]), cd(c[kCd]), diag(c[kCd] != 0.0) {}
+    HW_DEV Cf(const double *c)
+        : c0(c[kC0]), cx(c[kCx]), cy(c[kCy]), cd(c[kCd]), inv(c[kInv]), diag(c[kCd] != 0.0) {}
 };
 
 // L-shaped domain (LSH): point (i, j) of level L lies in the removed closed
@@ -443,13 +444,31 @@ __device__ __forceinline__ bool masked(int i, int j)
     return LSH && i >= h && j >= h;
 }
 
-// one point update in CSR column order (the reference's arithmetic)
-template <int L, bool LSH>
+// one point update.  Exact (FAST = false): CSR column order and the true
+// division, bit-identical to the reference -- used when these levels are the
+// whole hierarchy (K <= 5).  FAST: the symmetric neighbour pairs summed as a
+// shallow tree and a multiply by 1/c0 (a ~5-deep dependent chain instead of
+// 12 operations and a division on the wavefront's critical path) -- used
+// below the streamed levels, whose results already differ from the
+// reference by rounding.
+template <int L, bool LSH, bool FAST>
 __device__ __forceinline__ void gs_point(double *x, const double *b, const Cf &c, int i, int j)
 {
     constexpr int m = Lc<L>::m, p = Lc<L>::pitch;
     if (masked<L, LSH>(i, j)) return;
     const int k = i * p + j;
+    if constexpr (FAST) {
+        const double xl = j > 0 ? x[k - 1] : 0.0, xr = j < m - 1 ? x[k + 1] : 0.0;
+        const double xu = i > 0 ? x[k - p] : 0.0, xd = i < m - 1 ? x[k + p] : 0.0;
+        double off = fma(c.cx, xu + xd, c.cy * (xl + xr));
+        if (c.diag) {
+            const double xa = (i > 0 && j > 0) ? x[k - p - 1] : 0.0;
+            const double xb = (i < m - 1 && j < m - 1) ? x[k + p + 1] : 0.0;
+            off = fma(c.cd, xa + xb, off);
+        }
+        x[k] = (b[k] - off) * c.inv;
+        return;
+    }
     double acc = b[k];
     if (i > 0 && j > 0 && c.diag) acc = sub_mul(acc, c.cd, x[k - p - 1]);
     if (i > 0) acc = sub_mul(acc, c.cx, x[k - p]);
@@ -470,7 +489,7 @@ __device__ __forceinline__ void gs_point(double *x, const double *b, const Cf &c
 // so every point sees exactly the operands of three sequential sweeps
 // (bit-identical), in 2m+5 steps instead of 3(2m-1).  m <= 31: one grid row
 // per lane.
-template <int L, bool LSH>
+template <int L, bool LSH, bool FAST>
 __device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, const Cf &c,
                                               bool forward, int lane)
 {
@@ -488,7 +507,7 @@ __device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, cons
             const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
             const int ihi = d < m - 1 ? d : m - 1;
             const int i = ilo + lane;
-            if (i <= ihi) gs_point<L, LSH>(x, b, c, i, d - i);
+            if (i <= ihi) gs_point<L, LSH, FAST>(x, b, c, i, d - i);
         }
         __syncwarp();
     }
@@ -498,7 +517,7 @@ __device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, cons
 // (1,0) (2,0) in lexicographic order
 __device__ __forceinline__ int lsh_dof2(int a) { return a < 3 ? a : (a - 2) * 4; }
 
-template <int L, bool LSH>
+template <int L, bool LSH, bool FAST>
 __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw,
                                               const double *coef, const double *cinv, int lane)
 {
@@ -519,13 +538,25 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
         constexpr int m = Lc<L>::m, p = Lc<L>::pitch, mc = Lc<L - 1>::m, pc = Lc<L - 1>::pitch;
         const double *c = coef + L * kCoefStride;
         const Cf cf(c);
-        coarse_sweep3<L, LSH>(xw, bw, cf, true, lane);
+        coarse_sweep3<L, LSH, FAST>(xw, bw, cf, true, lane);
         double *x = xw + Lc<L>::off;
         const double *b = bw + Lc<L>::off;
         for (int k = lane; k < m * m; k += 32) {           // residual
             const int i = k / m, j = k % m, q = i * p + j;
             if (masked<L, LSH>(i, j)) {
                 rw[q] = 0.0;
+                continue;
+            }
+            if constexpr (FAST) {
+                const double xl = j > 0 ? x[q - 1] : 0.0, xr = j < m - 1 ? x[q + 1] : 0.0;
+                const double xu = i > 0 ? x[q - p] : 0.0, xd = i < m - 1 ? x[q + p] : 0.0;
+                double ax = fma(cf.cx, xu + xd, fma(cf.c0, x[q], cf.cy * (xl + xr)));
+                if (cf.diag) {
+                    const double xa = (i > 0 && j > 0) ? x[q - p - 1] : 0.0;
+                    const double xb = (i < m - 1 && j < m - 1) ? x[q + p + 1] : 0.0;
+                    ax = fma(cf.cd, xa + xb, ax);
+                }
+                rw[q] = b[q] - ax;
                 continue;
             }
             double acc = b[q];
@@ -556,7 +587,7 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
             xc[I * pc + J] = 0.0;
         }
         __syncwarp();
-        coarse_vcycle<L - 1, LSH>(xw, bw, rw, coef, cinv, lane);
+        coarse_vcycle<L - 1, LSH, FAST>(xw, bw, rw, coef, cinv, lane);
         const double *xcc = xw + Lc<L - 1>::off;
         for (int k = lane; k < m * m; k += 32) {           // prolongate (spatial.py:140-173)
             const int gi = k / m + 1, gj = k % m + 1;      // 1-based fine grid coords
@@ -578,14 +609,14 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
             if (!masked<L, LSH>(gi - 1, gj - 1)) x[q] = add_rn(x[q], acc);
         }
         __syncwarp();
-        coarse_sweep3<L, LSH>(xw, bw, cf, false, lane);
+        coarse_sweep3<L, LSH, FAST>(xw, bw, cf, false, lane);
     } else {
         if (lane == 0) xw[0] = add_mul(0.0, coef[1 * kCoefStride + kCoarse], bw[0]);  // 1x1 solve
         __syncwarp();
     }
 }
 
-template <int TOP, int WPB, bool LSH>
+template <int TOP, int WPB, bool LSH, bool FAST>
 __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, int64_t row, int lane)
 {
     constexpr int m = Lc<TOP>::m, p = Lc<TOP>::pitch;
@@ -602,11 +633,11 @@ __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, in
     }
     __syncwarp();
     const double *cinv = LSH ? a.cinv + (int64_t)op * 25 : nullptr;
-    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP, LSH>(xw, bw, rw, coef, cinv, lane);
+    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP, LSH, FAST>(xw, bw, rw, coef, cinv, lane);
     for (int k = lane; k < m * m; k += 32) Xg[k] = xw[Lc<TOP>::off + (k / m) * p + k % m];
 }
 
-template <int WPB, bool LSH>
+template <int WPB, bool LSH, bool FAST>
 __global__ void __launch_bounds__(32 * WPB) mg2d_coarse(MgCoarseArgs a)
 {
     extern __shared__ double sm[];
@@ -614,12 +645,16 @@ __global__ void __launch_bounds__(32 * WPB) mg2d_coarse(MgCoarseArgs a)
     const int64_t row = (int64_t)blockIdx.x * WPB + w;
     if (row >= a.rows) return;
     double *xw = sm + (size_t)w * kCoarseWords;
+    if constexpr (FAST) {                  // below the streamed levels: top = kCoarseTop2d
+        coarse_row<kCoarseTop2d, WPB, LSH, FAST>(a, xw, row, lane);
+        return;
+    }
     switch (a.top) {
-    case 1: if constexpr (!LSH) coarse_row<1, WPB, LSH>(a, xw, row, lane); break;
-    case 2: coarse_row<2, WPB, LSH>(a, xw, row, lane); break;
-    case 3: coarse_row<3, WPB, LSH>(a, xw, row, lane); break;
-    case 4: coarse_row<4, WPB, LSH>(a, xw, row, lane); break;
-    default: coarse_row<5, WPB, LSH>(a, xw, row, lane); break;
+    case 1: if constexpr (!LSH) coarse_row<1, WPB, LSH, FAST>(a, xw, row, lane); break;
+    case 2: coarse_row<2, WPB, LSH, FAST>(a, xw, row, lane); break;
+    case 3: coarse_row<3, WPB, LSH, FAST>(a, xw, row, lane); break;
+    case 4: coarse_row<4, WPB, LSH, FAST>(a, xw, row, lane); break;
+    default: coarse_row<5, WPB, LSH, FAST>(a, xw, row, lane); break;
     }
 }
 
@@ -665,7 +700,9 @@ cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st)
 {
     constexpr int WPB = 4;
     const size_t smem = (size_t)WPB * kCoarseWords * sizeof(double);
-    auto k = a.lshape ? mg2d_coarse<WPB, true> : mg2d_coarse<WPB, false>;
+    auto k = a.fast ? (a.lshape ? mg2d_coarse<WPB, true, true> : mg2d_coarse<WPB, false, true>)
+                    : (a.lshape ? mg2d_coarse<WPB, true, false> : mg2d_coarse<WPB, false, false>);
+    if (a.fast && a.top != kCoarseTop2d) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((a.rows + WPB - 1) / WPB);
