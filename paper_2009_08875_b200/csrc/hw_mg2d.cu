@@ -423,7 +423,7 @@ struct Lc {
 template <>
 struct Lc<0> { static constexpr int m = 0, pitch = 1, size = 0, off = 0; };
 constexpr int kCoarseStack = Lc<kCoarseTop2d>::off + Lc<kCoarseTop2d>::size;
-constexpr int kCoarseWords = 2 * kCoarseStack + Lc<kCoarseTop2d>::size;   // x, b, r
+constexpr int kCoarseWords = 2 * kCoarseStack;   // x, b
 
 // level coefficients in registers
 struct Cf {
@@ -518,8 +518,8 @@ __device__ __forceinline__ void coarse_sweep3(double *xw, const double *bw, cons
 __device__ __forceinline__ int lsh_dof2(int a) { return a < 3 ? a : (a - 2) * 4; }
 
 template <int L, bool LSH, bool FAST>
-__device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw,
-                                              const double *coef, const double *cinv, int lane)
+__device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, const double *coef,
+                                              const double *cinv, int lane)
 {
     if constexpr (LSH && L == 2) {
         // the L's coarsest level: dense inverse (multigrid.py:118,
@@ -541,12 +541,12 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
         coarse_sweep3<L, LSH, FAST>(xw, bw, cf, true, lane);
         double *x = xw + Lc<L>::off;
         const double *b = bw + Lc<L>::off;
-        for (int k = lane; k < m * m; k += 32) {           // residual
-            const int i = k / m, j = k % m, q = i * p + j;
-            if (masked<L, LSH>(i, j)) {
-                rw[q] = 0.0;
-                continue;
-            }
+        // residual r = b - A x, evaluated where the restriction needs it (no r
+        // array: the shared footprint per row drops to x and b, two rows per
+        // SM more); the exact path keeps the reference's CSR order
+        auto res = [&](int i, int j) -> double {
+            if (masked<L, LSH>(i, j)) return 0.0;
+            const int q = i * p + j;
             if constexpr (FAST) {
                 const double xl = j > 0 ? x[q - 1] : 0.0, xr = j < m - 1 ? x[q + 1] : 0.0;
                 const double xu = i > 0 ? x[q - p] : 0.0, xd = i < m - 1 ? x[q + p] : 0.0;
@@ -556,8 +556,7 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
                     const double xb = (i < m - 1 && j < m - 1) ? x[q + p + 1] : 0.0;
                     ax = fma(cf.cd, xa + xb, ax);
                 }
-                rw[q] = b[q] - ax;
-                continue;
+                return b[q] - ax;
             }
             double acc = b[q];
             if (i > 0 && j > 0 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[q - p - 1]);
@@ -567,27 +566,25 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, double *rw
             if (j < m - 1) acc = sub_mul(acc, c[kCy], x[q + 1]);
             if (i < m - 1) acc = sub_mul(acc, c[kCx], x[q + p]);
             if (i < m - 1 && j < m - 1 && c[kCd] != 0.0) acc = sub_mul(acc, c[kCd], x[q + p + 1]);
-            rw[q] = acc;
-        }
-        __syncwarp();
+            return acc;
+        };
         double *xc = xw + Lc<L - 1>::off, *bc = bw + Lc<L - 1>::off;
         for (int k = lane; k < mc * mc; k += 32) {         // restrict, R = P^T in CSR order
-            const int I = k / mc, J = k % mc;
-            const double *r0 = rw + (2 * I) * p + 2 * J;
-            const double *r1 = r0 + p, *r2 = r1 + p;
+            const int I = k / mc, J = k % mc, i0 = 2 * I, j0 = 2 * J;
             double acc = 0.0;
-            acc = add_mul(acc, 0.5, r0[0]);
-            acc = add_mul(acc, 0.5, r0[1]);
-            acc = add_mul(acc, 0.5, r1[0]);
-            acc = add_mul(acc, 1.0, r1[1]);
-            acc = add_mul(acc, 0.5, r1[2]);
-            acc = add_mul(acc, 0.5, r2[1]);
-            acc = add_mul(acc, 0.5, r2[2]);
+            acc = add_mul(acc, 0.5, res(i0, j0));
+            acc = add_mul(acc, 0.5, res(i0, j0 + 1));
+            acc = add_mul(acc, 0.5, res(i0 + 1, j0));
+            acc = add_mul(acc, 1.0, res(i0 + 1, j0 + 1));
+            acc = add_mul(acc, 0.5, res(i0 + 1, j0 + 2));
+            acc = add_mul(acc, 0.5, res(i0 + 2, j0 + 1));
+            acc = add_mul(acc, 0.5, res(i0 + 2, j0 + 2));
             bc[I * pc + J] = masked<L - 1, LSH>(I, J) ? 0.0 : acc;
-            xc[I * pc + J] = 0.0;
         }
+        __syncwarp();                                      // all reads of x_(L-1) region done
+        for (int k = lane; k < mc * mc; k += 32) xc[(k / mc) * pc + k % mc] = 0.0;
         __syncwarp();
-        coarse_vcycle<L - 1, LSH, FAST>(xw, bw, rw, coef, cinv, lane);
+        coarse_vcycle<L - 1, LSH, FAST>(xw, bw, coef, cinv, lane);
         const double *xcc = xw + Lc<L - 1>::off;
         for (int k = lane; k < m * m; k += 32) {           // prolongate (spatial.py:140-173)
             const int gi = k / m + 1, gj = k % m + 1;      // 1-based fine grid coords
@@ -621,7 +618,6 @@ __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, in
 {
     constexpr int m = Lc<TOP>::m, p = Lc<TOP>::pitch;
     double *bw = xw + kCoarseStack;
-    double *rw = bw + kCoarseStack;
     const int op = a.row_op ? a.row_op[row] : a.op;
     const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
     const double *Bg = a.B + row * a.ldB;
@@ -633,7 +629,7 @@ __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, in
     }
     __syncwarp();
     const double *cinv = LSH ? a.cinv + (int64_t)op * 25 : nullptr;
-    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP, LSH, FAST>(xw, bw, rw, coef, cinv, lane);
+    for (int cyc = 0; cyc < a.ncyc; ++cyc) coarse_vcycle<TOP, LSH, FAST>(xw, bw, coef, cinv, lane);
     for (int k = lane; k < m * m; k += 32) Xg[k] = xw[Lc<TOP>::off + (k / m) * p + k % m];
 }
 
