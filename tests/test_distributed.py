@@ -99,7 +99,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _gloo_worker(rank, world, port, outdir, d, J, K):
+def _gloo_worker(rank, world, port, outdir, d, J, K, domain="square"):
     import sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -107,7 +107,8 @@ def _gloo_worker(rank, world, port, outdir, d, J, K):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        O, system, f, eps, ref = _oracle_case(d, J, K)
+        O, system, f, eps, ref = _oracle_case(d, J, K, "lshape" if domain == "L" else "uniform",
+                                              domain=domain)
         states, W, res = _run_slabs(system, f, eps, world, D.TorchComm(), [rank])
         np.save(os.path.join(outdir, f"w{rank}.npy"), W[0].numpy())
         np.save(os.path.join(outdir, f"its{rank}.npy"), np.array([res.iterations]))
@@ -115,14 +116,15 @@ def _gloo_worker(rank, world, port, outdir, d, J, K):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_two_ranks_match_oracle_bitwise(world):
+@pytest.mark.parametrize("world,domain", [(2, "square"), (2, "L")])
+def test_gloo_two_ranks_match_oracle_bitwise(world, domain):
     d, J, K = 2, 4, 4
     port = _free_port()
     with tempfile.TemporaryDirectory() as tmp:
-        torch.multiprocessing.spawn(_gloo_worker, args=(world, port, tmp, d, J, K), nprocs=world,
-                                    join=True)
-        O, system, f, eps, ref = _oracle_case(d, J, K)
+        torch.multiprocessing.spawn(_gloo_worker, args=(world, port, tmp, d, J, K, domain),
+                                    nprocs=world, join=True)
+        O, system, f, eps, ref = _oracle_case(d, J, K, "lshape" if domain == "L" else "uniform",
+                                              domain=domain)
         parts = [np.load(os.path.join(tmp, f"w{r}.npy")) for r in range(world)]
         its = [int(np.load(os.path.join(tmp, f"its{r}.npy"))[0]) for r in range(world)]
     assert its == [ref.iterations] * world
