@@ -99,26 +99,25 @@ __device__ __forceinline__ void sweep_smem(double *x, const double *b, double oc
 }
 
 // r = b - A x on level L; restrict to level L-1 (zeroing its iterate)
+// (the three residuals a coarse point needs are evaluated where they are
+// used: no r array in shared memory)
 template <int L>
-__device__ __forceinline__ void residual_restrict(double *xw, double *bw, double *rw,
-                                                  const double *c, int lane)
+__device__ __forceinline__ void residual_restrict(double *xw, double *bw, const double *c, int lane)
 {
     constexpr int n = Lv<L>::n, nc = Lv<L - 1>::n;
     const double *x = xw + Lv<L>::off, *b = bw + Lv<L>::off;
-    for (int j = lane; j < n; j += 32) {
+    auto res = [&](int j) -> double {
         double acc = b[Lv<L>::at(j)];
         if (j > 0) acc = fma(-c[kCy], x[Lv<L>::at(j - 1)], acc);
         acc = fma(-c[kC0], x[Lv<L>::at(j)], acc);
         if (j < n - 1) acc = fma(-c[kCy], x[Lv<L>::at(j + 1)], acc);
-        rw[Lv<L>::at(j)] = acc;
-    }
-    __syncwarp();
+        return acc;
+    };
     double *xc = xw + Lv<L - 1>::off, *bc = bw + Lv<L - 1>::off;
-    for (int i = lane; i < nc; i += 32) {
-        bc[Lv<L - 1>::at(i)] = fma(0.5, rw[Lv<L>::at(2 * i)] + rw[Lv<L>::at(2 * i + 2)],
-                                   rw[Lv<L>::at(2 * i + 1)]);
-        xc[Lv<L - 1>::at(i)] = 0.0;
-    }
+    for (int i = lane; i < nc; i += 32)
+        bc[Lv<L - 1>::at(i)] = fma(0.5, res(2 * i) + res(2 * i + 2), res(2 * i + 1));
+    __syncwarp();
+    for (int i = lane; i < nc; i += 32) xc[Lv<L - 1>::at(i)] = 0.0;
     __syncwarp();
 }
 
@@ -156,13 +155,12 @@ __device__ __forceinline__ void smooth_level(double *xw, double *bw, const doubl
 // pre-smoothing + restriction from level L down, the 1x1 coarse solve, then
 // prolongation + post-smoothing back up to L (all in shared memory)
 template <int L>
-__device__ __forceinline__ void down_from(double *xw, double *bw, double *rw, const double *coef,
-                                          int lane)
+__device__ __forceinline__ void down_from(double *xw, double *bw, const double *coef, int lane)
 {
     if constexpr (L >= 2) {
         smooth_level<L>(xw, bw, coef, true, lane);
-        residual_restrict<L>(xw, bw, rw, coef + L * kCoefStride, lane);
-        down_from<L - 1>(xw, bw, rw, coef, lane);
+        residual_restrict<L>(xw, bw, coef + L * kCoefStride, lane);
+        down_from<L - 1>(xw, bw, coef, lane);
         prolongate_smem<L>(xw, lane);
         smooth_level<L>(xw, bw, coef, false, lane);
     } else {
@@ -184,7 +182,6 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_smem(Mg1dArgs a, int words)
     constexpr int ntot = Lv<K>::off + Lv<K>::size;
     double *xw = sm + (size_t)w * words;
     double *bw = xw + ntot;
-    double *rw = bw + ntot;
     const int op = a.row_op ? a.row_op[row] : a.op;
     const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
     constexpr int nK = Lv<K>::n;
@@ -195,7 +192,7 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_smem(Mg1dArgs a, int words)
         xw[Lv<K>::off + Lv<K>::at(k)] = 0.0;
     }
     __syncwarp();
-    for (int cyc = 0; cyc < a.ncyc; ++cyc) down_from<K>(xw, bw, rw, coef, lane);
+    for (int cyc = 0; cyc < a.ncyc; ++cyc) down_from<K>(xw, bw, coef, lane);
     for (int k = lane; k < nK; k += 32) Xg[k] = xw[Lv<K>::off + Lv<K>::at(k)];
 }
 
@@ -203,7 +200,7 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_smem(Mg1dArgs a, int words)
 // finest level in registers (K >= 6)
 // ---------------------------------------------------------------------------
 template <int K, int WPB>
-__global__ void __launch_bounds__(32 * WPB) mg1d_reg(Mg1dArgs a, int words)
+__global__ void __launch_bounds__(32 * WPB, 1) mg1d_reg(Mg1dArgs a, int words)
 {
     constexpr int CF = 1 << (K - 5);                    // points per lane, finest level
     constexpr int NC = CF / 2;                          // coarse points per lane (level K-1)
@@ -214,7 +211,6 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_reg(Mg1dArgs a, int words)
     constexpr int ntot = Lv<K - 1>::off + Lv<K - 1>::size;   // levels 1..K-1
     double *xw = sm + (size_t)w * words;
     double *bw = xw + ntot;
-    double *rw = bw + ntot;                             // scratch of level K-1
     const int op = a.row_op ? a.row_op[row] : a.op;
     const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
     const double *cK = coef + K * kCoefStride;
@@ -237,48 +233,46 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_reg(Mg1dArgs a, int words)
 #pragma unroll
     for (int k = 1; k < CF; ++k) gam *= beta;
 
-    // one GS sweep on the register-resident finest level.  The lane's chunk
-    // is split into NS independent sub-chunks (ILP); sub-chunk and lane
-    // carries are combined afterwards (x = y + beta^(pos+1) * carry).
     constexpr int NS = CF >= 16 ? 4 : (CF >= 4 ? 2 : 1);
     constexpr int SC = CF / NS;
     double bsc = beta;                                  // beta^SC
 #pragma unroll
     for (int k = 1; k < SC; ++k) bsc *= beta;
+    // GS sweep on the register-resident finest level, in three passes over
+    // the lane's chunk: (1) p_k = (b_k - c x_k+-1^old) / c0 in place (the
+    // neighbour is read before it is overwritten; no separate p array), (2) the
+    // zero-carry chunk end from NS independent sub-chunk recurrences, (3)
+    // after the lane carries (exact warp scan) the recurrence x_k = p_k +
+    // beta x_k-+1 again from each sub-chunk's true carry-in.
     auto sweep = [&](bool forward) {
-        const double xr = __shfl_down_sync(0xffffffffu, x[0], 1);        // next lane, old
-        const double xl = __shfl_up_sync(0xffffffffu, x[CF - 1], 1);     // previous lane, old
         double e[NS];                                   // sub-chunk end values (zero carry-in)
         if (forward) {
-            double p[CF];
+            const double xr = __shfl_down_sync(0xffffffffu, x[0], 1);    // next lane, old
 #pragma unroll
             for (int k = 0; k < CF; ++k) {
                 const double xn = (k + 1 < CF) ? x[k + 1] : (tail ? 0.0 : xr);
-                p[k] = fma(-oc, xn, b[k]) * inv;
+                x[k] = fma(-oc, xn, b[k]) * inv;
             }
 #pragma unroll
             for (int q = 0; q < NS; ++q) {
                 double y = 0.0;
 #pragma unroll
-                for (int k = q * SC; k < (q + 1) * SC; ++k) { y = fma(beta, y, p[k]); x[k] = y; }
+                for (int k = q * SC; k < (q + 1) * SC; ++k) y = fma(beta, y, x[k]);
                 e[q] = y;
             }
         } else {
-            double p[CF];
+            const double xl = __shfl_up_sync(0xffffffffu, x[CF - 1], 1);  // previous lane, old
 #pragma unroll
-            for (int k = 0; k < CF; ++k) {
+            for (int k = CF - 1; k >= 0; --k) {
                 const double xn = (k > 0) ? x[k - 1] : (lane == 0 ? 0.0 : xl);
-                p[k] = fma(-oc, xn, b[k]) * inv;
+                x[k] = fma(-oc, xn, b[k]) * inv;
             }
-            if (tail) p[CF - 1] = 0.0;                  // phantom: x stays 0
+            if (tail) x[CF - 1] = 0.0;                  // phantom: x stays 0
 #pragma unroll
             for (int q = 0; q < NS; ++q) {              // sub-chunk q = points CF-1-q*SC downwards
                 double y = 0.0;
 #pragma unroll
-                for (int k = CF - 1 - q * SC; k > CF - 1 - (q + 1) * SC; --k) {
-                    y = fma(beta, y, p[k]);
-                    x[k] = y;
-                }
+                for (int k = CF - 1 - q * SC; k > CF - 1 - (q + 1) * SC; --k) y = fma(beta, y, x[k]);
                 e[q] = y;
             }
         }
@@ -299,15 +293,15 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_reg(Mg1dArgs a, int words)
         if (forward ? lane == 0 : lane == 31) carry = 0.0;
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
-            double bp = beta;                           // beta^(pos in sub-chunk + 1)
+            double y = carry;
             if (forward) {
 #pragma unroll
-                for (int k = q * SC; k < (q + 1) * SC; ++k) { x[k] = fma(bp, carry, x[k]); bp *= beta; }
+                for (int k = q * SC; k < (q + 1) * SC; ++k) { y = fma(beta, y, x[k]); x[k] = y; }
             } else {
 #pragma unroll
                 for (int k = CF - 1 - q * SC; k > CF - 1 - (q + 1) * SC; --k) {
-                    x[k] = fma(bp, carry, x[k]);
-                    bp *= beta;
+                    y = fma(beta, y, x[k]);
+                    x[k] = y;
                 }
             }
             carry = fma(bsc, carry, e[q]);              // carry into sub-chunk q+1
@@ -342,7 +336,7 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_reg(Mg1dArgs a, int words)
             }
             __syncwarp();
         }
-        down_from<K - 1>(xw, bw, rw, coef, lane);
+        down_from<K - 1>(xw, bw, coef, lane);
         // prolongate into the registers: fine j = lane CF + k
         {
             const double *xc = xw + Lv<K - 1>::off;
@@ -370,12 +364,11 @@ __global__ void __launch_bounds__(32 * WPB) mg1d_reg(Mg1dArgs a, int words)
         if (lane * CF + k < nK) Xg[k] = x[k];
 }
 
-template <int K>
+template <int K, int WPB = 8>
 static cudaError_t launch_reg(const Mg1dArgs &a, cudaStream_t st)
 {
-    constexpr int WPB = 8;
     const int ntot = Lv<K - 1>::off + Lv<K - 1>::size;
-    const int words = 2 * ntot + Lv<K - 1>::size + 1;
+    const int words = 2 * ntot + 1;
     const size_t smem = (size_t)WPB * words * sizeof(double);
     auto k = mg1d_reg<K, WPB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -391,7 +384,7 @@ static cudaError_t launch_smem(const Mg1dArgs &a, cudaStream_t st)
 {
     constexpr int WPB = 4;
     const int ntot = Lv<K>::off + Lv<K>::size;
-    const int words = 2 * ntot + Lv<K>::size + 1;
+    const int words = 2 * ntot + 1;
     const size_t smem = (size_t)WPB * words * sizeof(double);
     auto k = mg1d_smem<K, WPB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
