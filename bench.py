@@ -186,6 +186,13 @@ def diffusion_of(cfg, d):
     return 0.25 * np.eye(2) if domain_of(cfg) == "L" else np.eye(d)
 
 
+def dof_fraction(cfg, d, K, n_x):
+    """Algorithmic bytes count the dofs: the L-shaped domain's kernels run on
+    the embedded (2^K-1)^2 grid, whose removed quadrant (1/4) carries no
+    information -- scale the grid-based byte counts by N_x / (2^K-1)^2."""
+    return n_x / (2 ** K - 1) ** d if domain_of(cfg) == "L" else 1.0
+
+
 def workload_label(cfg, d, J, K, n_t, n_x, world=1):
     if cfg == 5:
         return (f"cfg5: 2D L-shaped heat (mapped, D=I/4), J={J} (N_t={n_t}), K={K} "
@@ -335,6 +342,8 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dbytes, dn) = dom
+    dof_frac = dof_fraction(args.config, d, K, n_x)
+    dbytes *= dof_frac
     achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
@@ -343,8 +352,8 @@ def run_ours(args):
             rec = json.load(fh).get(dname)
         if rec:   # measured dram bytes / algorithmic bytes, scaled to this run's launches
             traffic = rec["traffic_over_algorithmic"] * dbytes / max(dn, 1)
-    model = model_bytes_per_iteration(d, J, K)
-    impl_b = impl_bytes_per_iteration(d, J, K)
+    model = model_bytes_per_iteration(d, J, K) * dof_frac
+    impl_b = impl_bytes_per_iteration(d, J, K) * dof_frac
     it_s = (ms_max / 1e3) / total_its
 
     # end-to-end through the C ABI with host buffers
@@ -503,9 +512,11 @@ def run_slab(args):
     peak, peak_src = measured_peaks()
     dom = max(prof.items(), key=lambda kv: kv[1][0])
     dname, (dms, dbytes, dn) = dom
+    dof_frac = dof_fraction(args.config, d, K, n_x)
+    dbytes *= dof_frac
     achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
-    model = model_bytes_per_iteration(d, J, K)
-    impl_b = impl_bytes_per_iteration(d, J, K)
+    model = model_bytes_per_iteration(d, J, K) * dof_frac
+    impl_b = impl_bytes_per_iteration(d, J, K) * dof_frac
     it_s = (ms_max / 1e3) / total_its
     if rank == 0:
         line = {

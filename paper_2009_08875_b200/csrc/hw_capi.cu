@@ -390,8 +390,9 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
 static int wavelet(hwg_ctx *c, const double *X, double *Y, double *S1, double *S2, bool tr,
                    cudaStream_t st, int64_t nx = 0)
 {
+    const bool grid = !nx || nx == c->nx;          // grid layout: skip the L's zero quadrant
     CK(wavelet_apply(X, Y, S1, S2, c->J, c->scale.data(), c->nt, nx ? nx : c->nx, tr, st,
-                     &c->launches));
+                     &c->launches, grid && c->domain ? c->m : 0, c->grid.lm));
     return HWG_OK;
 }
 

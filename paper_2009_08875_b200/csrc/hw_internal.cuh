@@ -68,9 +68,11 @@ struct Mg1dArgs {
 cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
 
 // ---- hw_wavelet.cu -------------------------------------------------------
+// mask_n > 0: columns are points of an mask_n x mask_n grid whose quadrant
+// a, b >= mask_lm is zero (the L-shaped domain): written, never read
 cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
                           const double *scale, int64_t nt, int64_t nx, bool transpose,
-                          cudaStream_t st, int64_t *launches);
+                          cudaStream_t st, int64_t *launches, int mask_n = 0, int mask_lm = 0);
 cudaError_t launch_syn_stage(int j, double s, const double *C, int64_t c0, const double *Dm,
                              int64_t d0, double *Y, int64_t f0, int64_t nf, int64_t nx,
                              cudaStream_t st);

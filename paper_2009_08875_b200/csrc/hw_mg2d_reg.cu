@@ -65,6 +65,18 @@ HW_DEV void cp_async16s(unsigned saddr, const void *gmem)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
 HW_DEV unsigned smem_u32(const void *p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+// zero-filling variants: `skip` writes zeros without reading global memory
+// (the L-shaped domain's removed quadrant, which holds zeros anyway)
+HW_DEV void cp_async16s(unsigned saddr, const void *gmem, bool skip)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+                 "r"(skip ? 0 : 16));
+}
+HW_DEV void cp_async8s(unsigned saddr, const void *gmem, bool skip)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
+                 "r"(skip ? 0 : 8));
+}
 
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 
@@ -259,17 +271,19 @@ struct RegPass {
 #pragma unroll
                 for (int k = 0; k < P / 2; ++k) {
                     const int q = tid + k * NT;              // pair (2q, 2q+1)
+                    const bool skip = LSH && i >= m && 2 * q >= m;   // removed quadrant
                     if (k < P / 2 - 1 || tid < NT - 1)
-                        cp_async16s(sa + 16u * k * NT, row0 + 2 * q);
+                        cp_async16s(sa + 16u * k * NT, row0 + 2 * q, skip);
                     else                                     // column n-1 only (n is a pad)
-                        cp_async8s(sa + 16u * k * NT, row0 + 2 * q);
+                        cp_async8s(sa + 16u * k * NT, row0 + 2 * q, skip);
                 }
             } else {
                 const double *g = row0 + tid;
                 const unsigned sa = smem_u32(slot + cpo);
 #pragma unroll
                 for (int k = 0; k < P; ++k)
-                    if (k < P - 1 || tid < NT - 1) cp_async8s(sa + 8u * koff(k), g + k * NT);
+                    if (k < P - 1 || tid < NT - 1)
+                        cp_async8s(sa + 8u * koff(k), g + k * NT, LSH && i >= m && tid + k * NT >= m);
             }
         } else {
             const unsigned sa = smem_u32(slot + phys(2 * tid));
@@ -279,7 +293,7 @@ struct RegPass {
                 const unsigned d = sa + 16u * k * NT;
                 if constexpr (LR == 0) {                     // columns (2q, 2q+1)
                     if (k < P / 2 - 1 || tid < NT - 1) {
-                        cp_async16s(d, row0 - 2 * q - 1);
+                        cp_async16s(d, row0 - 2 * q - 1, LSH && i <= m && 2 * q + 1 <= m);
                     } else {                                 // (n-1, n): column n-1 only;
                         cp_async8s(d + 8u, row0 - 2 * q);
                         // the pad n: the slot may last have held a parity-1
@@ -287,7 +301,7 @@ struct RegPass {
                         slot[phys(2 * q)] = 0.0;
                     }
                 } else {                                     // columns (2q-1, 2q)
-                    if (k > 0 || tid > 0) cp_async16s(d, row0 - 2 * q);
+                    if (k > 0 || tid > 0) cp_async16s(d, row0 - 2 * q, LSH && i <= m && 2 * q <= m);
                     else cp_async8s(d, row0);                // (-1, 0): column 0 only
                 }
             }
@@ -308,9 +322,11 @@ struct RegPass {
         }
         const double *g = Xcg + (int64_t)(m - 1 - ic) * m + (m - 1) - tid;
         const unsigned sa = smem_u32(slot);
+        constexpr int mc = (m - 1) / 2;                      // coarse removed quadrant (reversed)
 #pragma unroll
         for (int k = 0; k < (m + NT - 1) / NT; ++k)
-            if (tid + k * NT < m) cp_async8s(sa + 8u * k * NT, g - k * NT);
+            if (tid + k * NT < m)
+                cp_async8s(sa + 8u * k * NT, g - k * NT, LSH && ic <= mc && tid + k * NT <= mc);
     }
     HW_DEV int bslot(int back) const { return sb >= back ? sb - back : sb + SM::NB - back; }
     // the group step t issues: b(t+3) (into b(t-4)'s slot), x0(t+4) (into

@@ -37,17 +37,34 @@ __device__ __forceinline__ double qb(double s, int k, int nw) { return s * (k ==
 // ---------------------------------------------------------------------------
 constexpr int kWavQP = 16, kWavBS = 256;
 
+// L-shaped domain on the embedded grid (side mn, removed quadrant a, b >= lm):
+// those columns are zero in and out, so they are written without being read
+struct ColMask {
+    int mn, lm;                       // mn = 0: no mask
+    HW_DEV bool operator()(int64_t i) const
+    {
+        return mn > 0 && (int)(i / mn) >= lm && (int)(i % mn) >= lm;
+    }
+};
+
 // synthesis stage j over the full prefix: pair q = fine nodes 2q, 2q+1
 __global__ void __launch_bounds__(kWavBS) wav_syn_pairs(const double *__restrict__ C,
                                                         const double *__restrict__ Dm,
                                                         double *__restrict__ Y, int j, double s,
-                                                        int64_t nx)
+                                                        int64_t nx, ColMask msk)
 {
     const int nw = 1 << (j - 1);
     const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
     if (i >= nx) return;
     const int q0 = blockIdx.y * kWavQP;
     const int q1 = min(q0 + kWavQP, nw + 1);
+    if (msk(i)) {
+        for (int q = q0; q < q1; ++q) {
+            if (q < nw) Y[(int64_t)(2 * q + 1) * nx + i] = 0.0;
+            Y[(int64_t)(2 * q) * nx + i] = 0.0;
+        }
+        return;
+    }
     double cq = C[(int64_t)q0 * nx + i];
     double dm = q0 >= 1 ? Dm[(int64_t)(q0 - 1) * nx + i] : 0.0;   // d[q-1]
 #pragma unroll 4
@@ -74,13 +91,20 @@ __global__ void __launch_bounds__(kWavBS) wav_syn_pairs(const double *__restrict
 __global__ void __launch_bounds__(kWavBS) wav_ana_pairs(const double *__restrict__ X,
                                                         double *__restrict__ Cout,
                                                         double *__restrict__ Dout, int j,
-                                                        double s, int64_t nx)
+                                                        double s, int64_t nx, ColMask msk)
 {
     const int nw = 1 << (j - 1), nf = (1 << j) + 1;
     const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
     if (i >= nx) return;
     const int r0 = blockIdx.y * kWavQP;
     const int r1 = min(r0 + kWavQP, nw + 1);
+    if (msk(i)) {
+        for (int r = r0; r < r1; ++r) {
+            if (2 * r + 1 < nf) Dout[(int64_t)r * nx + i] = 0.0;
+            Cout[(int64_t)r * nx + i] = 0.0;
+        }
+        return;
+    }
     double xm = r0 >= 1 ? X[(int64_t)(2 * r0 - 1) * nx + i] : 0.0;   // x[2r-1]
     double x0 = X[(int64_t)(2 * r0) * nx + i];                      // x[2r]
 #pragma unroll 4
@@ -236,8 +260,9 @@ cudaError_t launch_ana_stage(int j, double s, const double *X, int64_t x0, doubl
 // transpose) are scratch arrays with at least 2^(J-1)+1 rows.
 cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
                           const double *scale, int64_t nt, int64_t nx, bool transpose,
-                          cudaStream_t st, int64_t *launches)
+                          cudaStream_t st, int64_t *launches, int mask_n, int mask_lm)
 {
+    const ColMask msk{mask_n, mask_lm};
     if (J == 0) {
         return cudaMemcpyAsync(Y, X, (size_t)(nt * nx) * sizeof(double),
                                cudaMemcpyDeviceToDevice, st);
@@ -248,7 +273,7 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
             double *dst = ((J - j) % 2 == 0) ? Y : S1;
             const int64_t nc = (1LL << (j - 1)) + 1;
             wav_syn_pairs<<<pair_grid((1 << (j - 1)) + 1, nx), kWavBS, 0, st>>>(
-                src, X + nc * nx, dst, j, scale[j - 1], nx);
+                src, X + nc * nx, dst, j, scale[j - 1], nx, msk);
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
             ++*launches;
@@ -260,7 +285,7 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
             double *cdst = (j == 1) ? Y : (((J - j) % 2 == 0) ? S1 : S2);
             const int64_t nc = (1LL << (j - 1)) + 1;
             wav_ana_pairs<<<pair_grid((1 << (j - 1)) + 1, nx), kWavBS, 0, st>>>(
-                src, cdst, Y + nc * nx, j, scale[j - 1], nx);
+                src, cdst, Y + nc * nx, j, scale[j - 1], nx, msk);
             cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
             ++*launches;
