@@ -66,12 +66,21 @@ def load(build_if_missing=True):
     global _lib
     if _lib is not None:
         return _lib
+    alt = os.environ.get("HWG_LIB_PATH")      # A/B measurements of two builds
+    if alt:
+        _lib = _bind(C.CDLL(alt))
+        return _lib
     if not os.path.exists(LIB_PATH):
         if not build_if_missing:
             raise OSError(f"{LIB_PATH} is missing; run python -m paper_2009_08875_b200.build")
         from . import build
         build.build()
-    L = C.CDLL(LIB_PATH)
+    _lib = _bind(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def _bind(L):
+    """Declare the ctypes signatures of every exported entry point."""
     L.hwg_last_error.restype = C.c_char_p
     L.hwg_version.restype = C.c_int
     L.hwg_create.argtypes = [C.POINTER(HwgDesc), C.POINTER(_P)]
@@ -109,7 +118,6 @@ def load(build_if_missing=True):
         if name not in ("hwg_last_error", "hwg_version", "hwg_workspace_bytes",
                         "hwg_launch_count"):
             getattr(L, name).restype = C.c_int
-    _lib = L
     return L
 
 

@@ -120,7 +120,7 @@ struct RegPass {
     // ---- per-CTA / per-thread constants ----
     int tid, lane, warp;
     bool last;                            // owns column n (a zero pad)
-    double cx, cy, cd, inv, beta;
+    double cxs, cds, c0, inv, beta;       // cx/c0, cd/c0, c0, 1/c0, -cy/c0
     double bp[P];                         // beta^(k+1)
     double wl[LEV];                       // scan weights gamma^(2^l) (0 below lane 2^l)
     double gl;                            // gamma^lane
@@ -174,11 +174,11 @@ struct RegPass {
         const int64_t row = blockIdx.x;
         const int op = a.row_op ? a.row_op[row] : a.op;
         const double *cf = a.coef + ((int64_t)op * a.levels_p1 + a.level) * kCoefStride;
-        cx = cf[kCx];
-        cy = cf[kCy];
-        cd = cf[kCd];
         inv = cf[kInv];
-        beta = -cy * inv;
+        c0 = cf[kC0];
+        cxs = cf[kCx] * inv;
+        cds = cf[kCd] * inv;
+        beta = -cf[kCy] * inv;
         double q = 1.0;
 #pragma unroll
         for (int k = 0; k < P; ++k) { q *= beta; bp[k] = q; }
@@ -475,10 +475,12 @@ struct RegPass {
             const double ul = k ? u[k - 1] : uL;
             const double cr = k < P - 1 ? c[k + 1] : cR;
             const double dr = k < P - 1 ? d[k + 1] : dR;
-            const double e1 = fma(-cd, ul, b[k]);
-            const double e2 = u[k] + d[k];
-            const double e3 = fma(cd, dr, cy * cr);
-            yy = fma(beta, yy, (fma(-cx, e2, e1) - e3) * inv);
+            // p = (b - cd (ul + dr) - cx (u + d) - cy cr) / c0 with the
+            // coefficients pre-scaled by 1/c0 (7 FP64 operations per point)
+            double pv = fma(beta, cr, b[k] * inv);
+            pv = fma(-cds, ul + dr, pv);
+            pv = fma(-cxs, u[k] + d[k], pv);
+            yy = fma(beta, yy, pv);
             if (LSH && ((rm >> k) & 1u)) yy = 0.0;
             y[k] = yy;
         }
@@ -538,7 +540,8 @@ struct RegPass {
             for (int k = 0; k < P; ++k) {
                 const double d6r = k < P - 1 ? D[PAR][k + 1] : DR[PAR];
                 const double d5r = k < P - 1 ? D[Q][k + 1] : DR[Q];
-                R[k] = fma(-cy, d6r, fma(-cx, D[Q][k], -cd * d5r));
+                // residual / c0 (the coarse right-hand side is scaled back by c0)
+                R[k] = fma(beta, d6r, fma(-cxs, D[Q][k], -cds * d5r));
             }
             if constexpr (LSH) {
                 const unsigned rr = rmask(t - 6);
@@ -626,7 +629,7 @@ struct RegPass {
                         acc[q] += fma(0.5, r0 + r2, r1);
                     } else {                             // bottom of r/2-1, top of r/2
                         if (r >= 2 && (q < P / 2 - 1 || !last))
-                            Bcg[(int64_t)(r / 2 - 1) * m + q] = acc[q] + 0.5 * (r1 + r2);
+                            Bcg[(int64_t)(r / 2 - 1) * m + q] = c0 * (acc[q] + 0.5 * (r1 + r2));
                         acc[q] = 0.5 * (r0 + r1);
                     }
                 }
