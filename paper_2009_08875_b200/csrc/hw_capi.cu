@@ -287,6 +287,16 @@ static int64_t level_size(const hwg_ctx *c, int l)
 // X[r] = MG_op(B[r]) for rows [0, rows); row_op: device per-row operator or null
 // dot_y (optional): also dot_part[r] = <dot_y row r, X row r>, fused into the
 // last finest-level UP pass when that pass runs on mg2d_reg, else by row_dots
+// does operator op (or, op = -1, any operator) couple diagonal neighbours on
+// level l (c_d != 0)?  The register kernel drops those terms when none does.
+static int level_has_diag(const hwg_ctx *c, int l, int op)
+{
+    const int nops = c->J + 2;
+    for (int o = op < 0 ? 0 : op; o < (op < 0 ? nops : op + 1); ++o)
+        if (c->coef_host[((size_t)o * (c->K + 1) + l) * HWG_COEF_STRIDE + kCd] != 0.0) return 1;
+    return 0;
+}
+
 static bool mg_dot_fusable(const hwg_ctx *c)
 {
     return c->dim == 2 && c->K >= 6 && c->K <= 11 && c->mg_reg_ok;
@@ -336,6 +346,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.reg_ok = c->mg_reg_ok;
                 a.lshape = c->domain;
                 a.small_rows = c->small_rows;
+                a.diag = level_has_diag(c, l, ro ? -1 : op);
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
                 ProfScope ps(c, st, l == c->K ? 0 : 2,
                              8.0 * nr * (n2 * (a.zero_start ? 2 : 3) + m2));
@@ -368,6 +379,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.reg_ok = c->mg_reg_ok;
                 a.lshape = c->domain;
                 a.small_rows = c->small_rows;
+                a.diag = level_has_diag(c, l, ro ? -1 : op);
                 if (fuse && l == c->K && cyc == c->nv - 1) {
                     a.dot_y = dot_y + r0 * c->nx;
                     a.dot_part = dot_part + r0;

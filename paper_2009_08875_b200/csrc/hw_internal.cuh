@@ -24,6 +24,7 @@ struct MgStreamArgs {
     const double *dot_y;                // UP (mg2d_reg): dot_part[row] = <dot_y row, final X row>
     double *dot_part;
     int lshape;                         // mapped L-shaped domain (mg2d_reg only)
+    int diag;                           // some row's operator has c_d != 0 on this level
     int64_t small_rows;                 // mg2d_reg n = 1023: batches of <= small_rows rows
                                         // use P = 4, 256 threads (under-filled GPU)
 };

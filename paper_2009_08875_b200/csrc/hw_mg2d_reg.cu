@@ -101,7 +101,9 @@ struct RegSmem {
 
 // LB0 / LX0 (UP only): layout parity of grid row 0 of b / x0 (stage_row);
 // row i has parity L0 ^ (i & 1) because a grid row is n (odd) words long
-template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0, bool LSH>
+// DG: the operator has diagonal couplings (c_d != 0, every C_j = alpha A +
+// mu M); DG = false (K_x = A_x, a 5-point stencil) drops them at compile time
+template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0, bool LSH, bool DG>
 struct RegPass {
     static constexpr int NW = NT / 32;
     static constexpr int n = P * NT - 1;
@@ -478,7 +480,7 @@ struct RegPass {
             // p = (b - cd (ul + dr) - cx (u + d) - cy cr) / c0 with the
             // coefficients pre-scaled by 1/c0 (7 FP64 operations per point)
             double pv = fma(beta, cr, b[k] * inv);
-            pv = fma(-cds, ul + dr, pv);
+            if constexpr (DG) pv = fma(-cds, ul + dr, pv);
             pv = fma(-cxs, u[k] + d[k], pv);
             yy = fma(beta, yy, pv);
             if (LSH && ((rm >> k) & 1u)) yy = 0.0;
@@ -541,7 +543,8 @@ struct RegPass {
                 const double d6r = k < P - 1 ? D[PAR][k + 1] : DR[PAR];
                 const double d5r = k < P - 1 ? D[Q][k + 1] : DR[Q];
                 // residual / c0 (the coarse right-hand side is scaled back by c0)
-                R[k] = fma(beta, d6r, fma(-cxs, D[Q][k], -cds * d5r));
+                R[k] = DG ? fma(beta, d6r, fma(-cxs, D[Q][k], -cds * d5r))
+                          : fma(beta, d6r, -cxs * D[Q][k]);
             }
             if constexpr (LSH) {
                 const unsigned rr = rmask(t - 6);
@@ -690,20 +693,20 @@ struct RegPass {
     }
 };
 
-template <int P, int NT, bool DOWN, bool ZS, int LB, int LX, bool LSH>
+template <int P, int NT, bool DOWN, bool ZS, int LB, int LX, bool LSH, bool DG>
 HW_DEV void run_pass(const MgStreamArgs &a, double *sm)
 {
-    RegPass<P, NT, DOWN, ZS, LB, LX, LSH> p(a, sm);
+    RegPass<P, NT, DOWN, ZS, LB, LX, LSH, DG> p(a, sm);
     p.run();
     p.finish_dot(a);
 }
 
-template <int P, int NT, bool DOWN, bool ZS, int MINB, bool LSH>
+template <int P, int NT, bool DOWN, bool ZS, int MINB, bool LSH, bool DG>
 __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
 {
     extern __shared__ __align__(16) double sm[];
     if constexpr (DOWN) {
-        run_pass<P, NT, DOWN, ZS, 0, 0, LSH>(a, sm);
+        run_pass<P, NT, DOWN, ZS, 0, 0, LSH, DG>(a, sm);
     } else {
         // UP: layout parity of grid row 0 (stage_row) = 1 when local column 0
         // (global row n-1, column n-1) sits at a 16-byte boundary
@@ -715,11 +718,11 @@ __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
         };
         const int lb = parity(a.B, a.ldB), lx = parity(a.X, a.ldX);
         if (lb) {
-            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1, LSH>(a, sm);
-            else run_pass<P, NT, DOWN, ZS, 1, 0, LSH>(a, sm);
+            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1, LSH, DG>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 1, 0, LSH, DG>(a, sm);
         } else {
-            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1, LSH>(a, sm);
-            else run_pass<P, NT, DOWN, ZS, 0, 0, LSH>(a, sm);
+            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1, LSH, DG>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 0, 0, LSH, DG>(a, sm);
         }
     }
 }
@@ -728,7 +731,9 @@ template <int P, int NT, bool DOWN, bool ZS, int MINB>
 cudaError_t launch_reg_t(const MgStreamArgs &a, int64_t rows, cudaStream_t st)
 {
     const size_t smem = RegSmem<P, NT, DOWN, ZS>::total * sizeof(double);
-    auto k = a.lshape ? mg2d_reg<P, NT, DOWN, ZS, MINB, true> : mg2d_reg<P, NT, DOWN, ZS, MINB, false>;
+    auto k = a.lshape ? mg2d_reg<P, NT, DOWN, ZS, MINB, true, true>
+                      : (a.diag ? mg2d_reg<P, NT, DOWN, ZS, MINB, false, true>
+                                : mg2d_reg<P, NT, DOWN, ZS, MINB, false, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)rows, NT, smem, st>>>(a);
