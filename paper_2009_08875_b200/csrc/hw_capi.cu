@@ -56,7 +56,6 @@ struct hwg_ctx {
     hwg_desc d{};
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
-    int64_t small_rows = 0;             // see MgStreamArgs::small_rows
     int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
@@ -345,7 +344,6 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.zero_start = (l < c->K || cyc == 0) ? 1 : 0;
                 a.reg_ok = c->mg_reg_ok;
                 a.lshape = c->domain;
-                a.small_rows = c->small_rows;
                 a.diag = level_has_diag(c, l, ro ? -1 : op);
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
                 ProfScope ps(c, st, l == c->K ? 0 : 2,
@@ -378,7 +376,6 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.op = op;
                 a.reg_ok = c->mg_reg_ok;
                 a.lshape = c->domain;
-                a.small_rows = c->small_rows;
                 a.diag = level_has_diag(c, l, ro ? -1 : op);
                 if (fuse && l == c->K && cyc == c->nv - 1) {
                     a.dot_y = dot_y + r0 * c->nx;
@@ -555,7 +552,6 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         if (ev[0] == '0') c->mg_reg_ok = 0;
         else if (ev[0] == '4' && c->mg_reg_ok) c->mg_reg_ok = 2;   // P = 4 at n = 1023
         else if (ev[0] == '5' && c->mg_reg_ok) c->mg_reg_ok = 3;   // P = 4 for UP at n = 1023
-    if (const char *ev = getenv("HWG_REG_SMALL_ROWS")) c->small_rows = atoll(ev);
     if (const char *ev = getenv("HWG_COARSE_EXACT"))        // A/B switch for measurements
         if (ev[0] == '1') c->coarse_fast = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask

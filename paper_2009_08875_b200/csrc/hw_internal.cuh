@@ -25,8 +25,6 @@ struct MgStreamArgs {
     double *dot_part;
     int lshape;                         // mapped L-shaped domain (mg2d_reg only)
     int diag;                           // some row's operator has c_d != 0 on this level
-    int64_t small_rows;                 // mg2d_reg n = 1023: batches of <= small_rows rows
-                                        // use P = 4, 256 threads (under-filled GPU)
 };
 
 struct MgCoarseArgs {

@@ -759,7 +759,7 @@ cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cuda
     case 511: return launch_reg_n<8, 64, 1>(a, down, rows, st);
     case 1023:
         // HWG_MG_REG=4: P = 4 for both passes; =5: P = 4 for UP only (A/B)
-        if (a.reg_ok == 2 || (a.reg_ok == 3 && !down) || rows <= a.small_rows)
+        if (a.reg_ok == 2 || (a.reg_ok == 3 && !down))
             return launch_reg_n<4, 256, 1>(a, down, rows, st);
         return launch_reg_n<8, 128, 2>(a, down, rows, st);
     case 2047: return launch_reg_n<8, 256, 1>(a, down, rows, st);

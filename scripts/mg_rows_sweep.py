@@ -1,6 +1,7 @@
 """Per-row cost of one batched K_x multigrid apply vs batch size (the
 under-filled GPU of small time slabs), register kernel P = 8 x 128 threads
-(2 CTAs/SM) vs P = 4 x 256 threads (HWG_REG_SMALL_ROWS).
+(2 CTAs/SM) vs P = 4 x 256 threads (HWG_MG_REG=4).  Measured: the P = 4
+variant is slower at every batch size.
 
     python scripts/mg_rows_sweep.py [--K 10] [--rows 64 137 258 296 1025 2050]
 """
@@ -20,8 +21,8 @@ ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
 rmax = max(a.rows)
 ctxs = {}
-for name, env in (("P8x128", "0"), ("P4x256", str(10 ** 9))):
-    os.environ["HWG_REG_SMALL_ROWS"] = env
+for name, env in (("P8x128", "1"), ("P4x256", "4")):
+    os.environ["HWG_MG_REG"] = env
     ctxs[name] = GpuContext(2, 3, a.K, rows_max=rmax)
 n = (2 ** a.K - 1) ** 2
 B = torch.randn((rmax, n), dtype=torch.float64, device="cuda")
