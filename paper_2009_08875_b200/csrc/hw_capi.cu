@@ -83,6 +83,8 @@ struct hwg_ctx {
     // PCG vectors (lazy)
     double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
     double *fdev = nullptr, *wdev = nullptr;
+    cudaStream_t copy_stream = nullptr;   // hwg_solve_host: chunked host -> device copies
+    std::vector<cudaEvent_t> copy_events;
     int64_t bytes = 0;
     int64_t launches = 0;
     std::vector<void *> allocs;
@@ -448,14 +450,23 @@ static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
 
 // K_X = blockdiag[C_l A_x C_l] (system.py:242-276); dot_y (optional): also
 // the per-row partials of <dot_y, Y>, fused into the last multigrid pass
+// K_X on rows [r0, r0 + nr) only (K_X is row-local)
+static int kx_rows(hwg_ctx *c, const double *X, double *Y, int64_t r0, int64_t nr,
+                   cudaStream_t st, const double *dot_y, double *dot_part)
+{
+    const int64_t o = r0 * c->nx;
+    TRY(mg_apply(c, X + o, Y + o, nr, 0, c->row_op_kx + r0, st));
+    CK(launch_stencil_rows(Y + o, nullptr, c->G12 + o, c->grid, c->SM, c->SA, nr, st));
+    ++c->launches;
+    TRY(mg_apply(c, c->G12 + o, Y + o, nr, 0, c->row_op_kx + r0, st, dot_y ? dot_y + o : nullptr,
+                 dot_part ? dot_part + r0 : nullptr));
+    return HWG_OK;
+}
+
 static int kx(hwg_ctx *c, const double *X, double *Y, cudaStream_t st,
               const double *dot_y = nullptr, double *dot_part = nullptr)
 {
-    TRY(mg_apply(c, X, Y, c->nt, 0, c->row_op_kx, st));
-    CK(launch_stencil_rows(Y, nullptr, c->G12, c->grid, c->SM, c->SA, c->nt, st));
-    ++c->launches;
-    TRY(mg_apply(c, c->G12, Y, c->nt, 0, c->row_op_kx, st, dot_y, dot_part));
-    return HWG_OK;
+    return kx_rows(c, X, Y, 0, c->nt, st, dot_y, dot_part);
 }
 
 static cudaStream_t S(void *s) { return (cudaStream_t)s; }
@@ -649,6 +660,8 @@ int hwg_destroy(hwg_ctx *c)
     if (!c) return HWG_OK;
     prof_flush(c);
     for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->copy_events) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (void *p : c->allocs) cudaFree(p);
     if (c->hscal) cudaFreeHost(c->hscal);
     delete c;
@@ -825,10 +838,18 @@ int hwg_dot(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *
 
 }  // extern "C"
 
+// f arriving in row chunks: chunk k (rows [k rows, (k+1) rows)) is in place
+// once ev[k] has completed (hwg_solve_host's pipelined host -> device copy)
+struct StagedInput {
+    int n = 0;
+    int64_t rows = 0;
+    const cudaEvent_t *ev = nullptr;
+};
+
 // PCG on grid-layout f, w (hwg_pcg converts dof-layout operands)
 static int pcg_core(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
                     int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out,
-                    cudaStream_t st)
+                    cudaStream_t st, const StagedInput *staged = nullptr)
 {
     TRY(ensure_pcg(c));
     const int64_t N = c->N, nt = c->nt, nx = c->nx;
@@ -849,20 +870,43 @@ static int pcg_core(hwg_ctx *c, const double *f, double *w, double epsilon, doub
     CK(cudaMemsetAsync(w, 0, N * sizeof(double), st));
     // zero right-hand side returns immediately (solver.py:196-198)
     CK(cudaMemsetAsync(c->flag, 0, sizeof(int), st));
-    CK(launch_any_nonzero(f, N, c->flag, st));
-    ++c->launches;
     int hflag = 0;
-    CK(cudaMemcpyAsync(&hflag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (!hflag) {
-        push(out.residual_norms, 0, 0.0);
-        out.epsilon_used = epsilon;
-        return HWG_OK;
+    if (staged && staged->n > 1) {
+        // r = f and z = K_X r chunk by chunk as the rows arrive (K_X is
+        // row-local), overlapping the host -> device copy of the later rows
+        CK(cudaEventRecord(ev[1], st));
+        for (int k = 0; k < staged->n; ++k) {
+            const int64_t r0 = k * staged->rows, nr = std::min(staged->rows, nt - r0);
+            CK(cudaStreamWaitEvent(st, staged->ev[k], 0));
+            CK(launch_any_nonzero(f + r0 * nx, nr * nx, c->flag, st));
+            CK(cudaMemcpyAsync(c->r + r0 * nx, f + r0 * nx, nr * nx * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+            ++c->launches;
+            TRY(kx_rows(c, c->r, c->z, r0, nr, st, c->r, c->part));
+        }
+        CK(cudaEventRecord(ev[2], st));
+        CK(cudaMemcpyAsync(&hflag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!hflag) {
+            push(out.residual_norms, 0, 0.0);
+            out.epsilon_used = epsilon;
+            return HWG_OK;
+        }
+    } else {
+        CK(launch_any_nonzero(f, N, c->flag, st));
+        ++c->launches;
+        CK(cudaMemcpyAsync(&hflag, c->flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!hflag) {
+            push(out.residual_norms, 0, 0.0);
+            out.epsilon_used = epsilon;
+            return HWG_OK;
+        }
+        CK(cudaMemcpyAsync(c->r, f, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CK(cudaEventRecord(ev[1], st));
+        TRY(kx(c, c->r, c->z, st, c->r, c->part));       // r.z fused into K_X's last pass
+        CK(cudaEventRecord(ev[2], st));
     }
-    CK(cudaMemcpyAsync(c->r, f, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    CK(cudaEventRecord(ev[1], st));
-    TRY(kx(c, c->r, c->z, st, c->r, c->part));           // r.z fused into K_X's last pass
-    CK(cudaEventRecord(ev[2], st));
     CK(launch_tree(c->part, nt, c->tmp, c->scal + 0, st));
     ++c->launches;
     CK(cudaMemcpyAsync(c->hscal, c->scal, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -984,13 +1028,37 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
         TRY(dalloc(c, &c->fdev, c->N));
         TRY(dalloc(c, &c->wdev, c->N));
     }
-    CK(cudaMemcpyAsync(c->fdev, fhat_host, c->Nu * sizeof(double), cudaMemcpyHostToDevice, st));
+    // large problems: copy f-hat in row chunks on a second stream and start
+    // the (row-local) initial K_X on each chunk as it lands
+    StagedInput staged;
+    const int64_t chunk_rows = 256;
+    if (!c->domain && c->N >= (int64_t)1 << 26 && c->nt > chunk_rows) {
+        if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        const int n = (int)((c->nt + chunk_rows - 1) / chunk_rows);
+        while ((int)c->copy_events.size() < n + 1) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->copy_events.push_back(e);
+        }
+        CK(cudaEventRecord(c->copy_events[n], st));       // earlier work on fdev done
+        CK(cudaStreamWaitEvent(c->copy_stream, c->copy_events[n], 0));
+        for (int k = 0; k < n; ++k) {
+            const int64_t r0 = k * chunk_rows, nr = std::min(chunk_rows, c->nt - r0);
+            CK(cudaMemcpyAsync(c->fdev + r0 * c->nx, fhat_host + r0 * c->nx,
+                               nr * c->nx * sizeof(double), cudaMemcpyHostToDevice, c->copy_stream));
+            CK(cudaEventRecord(c->copy_events[k], c->copy_stream));
+        }
+        staged = StagedInput{n, chunk_rows, c->copy_events.data()};
+    } else {
+        CK(cudaMemcpyAsync(c->fdev, fhat_host, c->Nu * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
     const double *f = c->fdev;
     if (c->domain) {                          // dof layout -> grid layout (in place is not
         TRY(to_grid(c, c->fdev, c->Xg, c->nt, st));   // allowed: via Xg)
         f = c->Xg;
     }
-    int rc = pcg_core(c, f, c->wdev, epsilon, rtol, max_iterations, recompute_every, stats, st);
+    int rc = pcg_core(c, f, c->wdev, epsilon, rtol, max_iterations, recompute_every, stats, st,
+                      staged.n > 1 ? &staged : nullptr);
     if (rc != HWG_OK && rc != HWG_EMAXIT) return rc;
     const std::string msg = g_err;
     TRY(wavelet(c, c->wdev, c->U, c->T12, c->T12 + c->N, false, st));

@@ -393,3 +393,29 @@ def test_test_space_form_and_lanczos(name):
     assert r_ts.iterations == r_5.iterations
     w5 = r_5.w.array
     assert np.linalg.norm(r_ts.w.array - w5) <= 1e-10 * np.linalg.norm(w5)
+
+
+def test_solve_host_pipelined_copy_matches_device_solve():
+    """hwg_solve_host at a size where f-hat is copied in row chunks on a
+    second stream, the initial K_X running on each chunk as it lands
+    (N >= 2^26, N_t > 256): same iterations and a bit-identical u as the
+    device-resident hwg_pcg followed by W."""
+    J, K = 9, 9
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** 2
+    F = inputs.forcing("uniform", n_t, n_x)
+    asm = hw.assemble_system(hw.ProblemData(D=np.eye(2), c=0.0, u0=inputs.u0_sines), J, K,
+                             hw.SolveConfig(), forcing=F, host_rhs=False)
+    ctx = asm.ctx
+    f = asm.rhs.f_hat.array
+    w = torch.empty_like(f)
+    st, rc = ctx.pcg(f, w, 0.0, 1e-6)
+    assert rc == 0
+    u_dev = asm.wavelet.apply_array(w).cpu().numpy()
+    fh = torch.empty(f.shape, dtype=torch.float64, pin_memory=True)
+    fh.copy_(f)
+    uh = torch.empty(f.shape, dtype=torch.float64, pin_memory=True)
+    st2, rc2 = ctx.solve_host(fh.numpy(), uh.numpy(), 0.0, 1e-6)
+    assert rc2 == 0
+    assert st2["iterations"] == st["iterations"]
+    assert st2["residual_norms"] == st["residual_norms"]
+    assert np.array_equal(uh.numpy(), u_dev)
