@@ -114,7 +114,10 @@ typedef struct {
     double *residual_norms;   /* sqrt(rho_k), k = 0..iterations */
     double *alphas;           /* cg_alphas, iterations entries */
     double *betas;            /* cg_betas */
-    double ms_schur, ms_precond, ms_vector, ms_total;  /* wall_times */
+    double ms_schur, ms_precond, ms_vector, ms_total;  /* wall_times; the per-phase times
+                                * are only measured when iterations run as plain launches
+                                * (profiling on or HWG_GRAPH=0), else 0: by default each
+                                * iteration replays one captured CUDA graph */
     double epsilon_used;      /* the absolute tolerance actually applied */
 } hwg_pcg_stats;
 

@@ -84,6 +84,12 @@ struct hwg_ctx {
     double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
     double *fdev = nullptr, *wdev = nullptr;
     cudaStream_t copy_stream = nullptr;   // hwg_solve_host: chunked host -> device copies
+    int use_graph = 1;                    // PCG iterations replayed as a CUDA graph
+    cudaGraphExec_t graph_exec = nullptr; // one iteration (no recomputation) for graph_w
+    cudaStream_t capture_stream = nullptr;  // graphs are captured here (the caller's stream
+                                            // may be the legacy default stream)
+    const double *graph_w = nullptr;
+    int64_t graph_kernels = 0;
     std::vector<cudaEvent_t> copy_events;
     int64_t bytes = 0;
     int64_t launches = 0;
@@ -565,6 +571,8 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         else if (ev[0] == '5' && c->mg_reg_ok) c->mg_reg_ok = 3;   // P = 4 for UP at n = 1023
     if (const char *ev = getenv("HWG_COARSE_EXACT"))        // A/B switch for measurements
         if (ev[0] == '1') c->coarse_fast = 0;
+    if (const char *ev = getenv("HWG_GRAPH"))               // A/B switch for measurements
+        if (ev[0] == '0') c->use_graph = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask
     if (!c->mg_reg_ok && d.dim == 2 && d.K > kCoarseTop2d && (d.K > 10 || d.domain)) {
         delete c;
@@ -661,6 +669,8 @@ int hwg_destroy(hwg_ctx *c)
     prof_flush(c);
     for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : c->copy_events) cudaEventDestroy(e);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (void *p : c->allocs) cudaFree(p);
     if (c->hscal) cudaFreeHost(c->hscal);
@@ -838,6 +848,61 @@ int hwg_dot(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *
 
 }  // extern "C"
 
+// One PCG iteration without residual recomputation (solver.py:212-256):
+// q = S p, p.q, alpha, r -= alpha q, z = K_X r with r.z fused, beta, then
+// w += alpha p and p = z + beta p in one pass; the four scalars are copied to
+// the pinned host mirror.  Everything is stream-ordered and device-resident,
+// so the sequence can be captured as a CUDA graph.
+static int enqueue_iteration(hwg_ctx *c, double *w, cudaStream_t st)
+{
+    const int64_t N = c->N, nt = c->nt, nx = c->nx;
+    TRY(schur(c, c->p, c->q, st));
+    CK(launch_dot(c->p, c->q, nt, nx, c->part, c->tmp, c->scal + 1, st, &c->launches));
+    CK(launch_pcg_alpha(c->scal, st));
+    CK(launch_update_wr(w, c->r, c->p, c->q, c->scal, N, 0, 1, st));
+    c->launches += 2;
+    TRY(kx(c, c->r, c->z, st, c->r, c->part));
+    CK(launch_tree(c->part, nt, c->tmp, c->scal + 2, st));
+    ++c->launches;
+    CK(cudaMemcpyAsync(c->hscal + 1, c->scal + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(launch_pcg_beta(c->scal, st));
+    CK(launch_update_wp(w, c->p, c->z, c->scal, N, 1, st));
+    c->launches += 2;
+    CK(cudaMemcpyAsync(c->hscal + 3, c->scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    return HWG_OK;
+}
+
+// the iteration as an instantiated CUDA graph (captured once per w buffer):
+// ~300 dependent launches become one graph launch
+static int iteration_graph(hwg_ctx *c, double *w)
+{
+    if (c->graph_exec && c->graph_w == w) return HWG_OK;
+    if (c->graph_exec) {
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+    }
+    if (!c->capture_stream) CK(cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking));
+    cudaStream_t cs = c->capture_stream;
+    const int64_t l0 = c->launches;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    const int rc = enqueue_iteration(c, w, cs);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cs, &g);
+    const int64_t kernels = c->launches - l0;           // counted at each replay instead
+    c->launches = l0;
+    if (rc != HWG_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    CK(e);
+    const cudaError_t ei = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(ei);
+    c->graph_w = w;
+    c->graph_kernels = kernels;
+    return HWG_OK;
+}
+
 // f arriving in row chunks: chunk k (rows [k rows, (k+1) rows)) is in place
 // once ev[k] has completed (hwg_solve_host's pipelined host -> device copy)
 struct StagedInput {
@@ -926,13 +991,21 @@ static int pcg_core(hwg_ctx *c, const double *f, double *w, double epsilon, doub
         return HWG_OK;
     }
     CK(cudaMemcpyAsync(c->p, c->z, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    const bool graphs = c->use_graph && !c->prof;      // profiling events need plain launches
     for (int k = 1; k <= max_iterations; ++k) {
+      const bool recompute = (k % recompute_every) == 0;
+      if (graphs && !recompute) {
+        TRY(iteration_graph(c, w));                      // (re)captured when w changes
+        CK(cudaGraphLaunch(c->graph_exec, st));
+        c->launches += c->graph_kernels;
+        CK(cudaEventRecord(ev[6], st));
+        CK(cudaEventSynchronize(ev[6]));
+      } else {
         CK(cudaEventRecord(ev[1], st));
         TRY(schur(c, c->p, c->q, st));
         CK(cudaEventRecord(ev[2], st));
         CK(launch_dot(c->p, c->q, nt, nx, c->part, c->tmp, c->scal + 1, st, &c->launches));
         CK(launch_pcg_alpha(c->scal, st));
-        const bool recompute = (k % recompute_every) == 0;
         // r -= alpha q now; w += alpha p is deferred into the p update below
         // (one pass over p), except before a residual recomputation, which
         // needs the current w
@@ -964,6 +1037,7 @@ static int pcg_core(hwg_ctx *c, const double *f, double *w, double epsilon, doub
         out.ms_schur += a + cc;
         out.ms_vector += b;
         out.ms_precond += dd;
+      }
         const double pq = c->hscal[1], rho_new = c->hscal[2];
         const double alpha = c->hscal[3], beta = c->hscal[4];
         if (!(pq > 0)) {
