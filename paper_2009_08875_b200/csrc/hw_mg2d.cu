@@ -413,16 +413,21 @@ __global__ void __launch_bounds__(NT, 1) mg2d_stream(MgStreamArgs a)
 // Level L (m = 2^L - 1 points per direction) is stored with row pitch 2^L so
 // the anti-diagonal wavefront stride (pitch - 1 = m, odd) keeps a warp's
 // 64-bit shared accesses bank-conflict free.
+// Each level's block is a zero pad row, the m grid rows, a zero pad row; the
+// pad column (j = m) of every row is zero too, so every neighbour of a grid
+// point is an in-bounds word that reads 0 outside the grid (the FAST path
+// needs no boundary tests).  off = row 0.
 template <int L>
 struct Lc {
     static constexpr int m = (1 << L) - 1;
     static constexpr int pitch = 1 << L;
-    static constexpr int size = pitch * m;
-    static constexpr int off = Lc<L - 1>::off + Lc<L - 1>::size;
+    static constexpr int size = pitch * (m + 2);
+    static constexpr int base = Lc<L - 1>::base + Lc<L - 1>::size;
+    static constexpr int off = base + pitch;
 };
 template <>
-struct Lc<0> { static constexpr int m = 0, pitch = 1, size = 0, off = 0; };
-constexpr int kCoarseStack = Lc<kCoarseTop2d>::off + Lc<kCoarseTop2d>::size;
+struct Lc<0> { static constexpr int m = 0, pitch = 1, size = 0, base = 0, off = 0; };
+constexpr int kCoarseStack = Lc<kCoarseTop2d>::base + Lc<kCoarseTop2d>::size;
 constexpr int kCoarseWords = 2 * kCoarseStack;   // x, b
 
 // level coefficients in registers
@@ -500,26 +505,25 @@ __device__ __forceinline__ void coarse_sweep3_fast(double *x, const double *b, c
     constexpr int D = 2 * m - 1;
     const int i = lane < m ? lane : m - 1;
     const bool rowok = lane < m;
+    double *xr = x + i * p;
+    const double *br = b + i * p;
+    // column of sweep s at step tau: j = d - i, d = tau - 3 s (forward) or
+    // D - 1 - (tau - 3 s) (backward): one increment per step
+    int js[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) js[s] = FWD ? -3 * s - i : D - 1 + 3 * s - i;
     for (int tau = 0; tau < D + 6; ++tau) {
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
-            const int dd = tau - 3 * s;
-            const int d = FWD ? dd : D - 1 - dd;
-            const int j = d - i;
-            const bool ok = rowok && (unsigned)dd < (unsigned)D && (unsigned)j < (unsigned)m &&
-                            !masked<L, LSH>(i, j);
-            const int jc = j < 0 ? 0 : (j > m - 1 ? m - 1 : j);
-            const int k = i * p + jc;
-            const double xl = jc > 0 ? x[k - 1] : 0.0, xr = jc < m - 1 ? x[k + 1] : 0.0;
-            const double xu = i > 0 ? x[k - p] : 0.0, xd = i < m - 1 ? x[k + p] : 0.0;
-            double off = fma(c.cx, xu + xd, c.cy * (xl + xr));
-            if constexpr (DIAG) {
-                const double xa = (i > 0 && jc > 0) ? x[k - p - 1] : 0.0;
-                const double xb = (i < m - 1 && jc < m - 1) ? x[k + p + 1] : 0.0;
-                off = fma(c.cd, xa + xb, off);
-            }
-            const double v = (b[k] - off) * c.inv;
-            if (ok) x[k] = v;
+            const int j = js[s];
+            const bool ok = rowok && (unsigned)j < (unsigned)m && !masked<L, LSH>(i, j);
+            const int jc = min(max(j, 0), m - 1);       // in-bounds address for idle lanes
+            const double *xp = xr + jc;
+            double off = fma(c.cx, xp[-p] + xp[p], c.cy * (xp[-1] + xp[1]));
+            if constexpr (DIAG) off = fma(c.cd, xp[-p - 1] + xp[p + 1], off);
+            const double v = (br[jc] - off) * c.inv;
+            if (ok) xr[jc] = v;
+            js[s] = FWD ? j + 1 : j - 1;
         }
         __syncwarp();
     }
@@ -595,15 +599,9 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, const doub
         auto res = [&](int i, int j) -> double {
             if (masked<L, LSH>(i, j)) return 0.0;
             const int q = i * p + j;
-            if constexpr (FAST) {
-                const double xl = j > 0 ? x[q - 1] : 0.0, xr = j < m - 1 ? x[q + 1] : 0.0;
-                const double xu = i > 0 ? x[q - p] : 0.0, xd = i < m - 1 ? x[q + p] : 0.0;
-                double ax = fma(cf.cx, xu + xd, fma(cf.c0, x[q], cf.cy * (xl + xr)));
-                if (cf.diag) {
-                    const double xa = (i > 0 && j > 0) ? x[q - p - 1] : 0.0;
-                    const double xb = (i < m - 1 && j < m - 1) ? x[q + p + 1] : 0.0;
-                    ax = fma(cf.cd, xa + xb, ax);
-                }
+            if constexpr (FAST) {                        // zero pads: no boundary tests
+                double ax = fma(cf.cx, x[q - p] + x[q + p], fma(cf.c0, x[q], cf.cy * (x[q - 1] + x[q + 1])));
+                if (cf.diag) ax = fma(cf.cd, x[q - p - 1] + x[q + p + 1], ax);
                 return b[q] - ax;
             }
             double acc = b[q];
@@ -656,7 +654,8 @@ __device__ __forceinline__ void coarse_vcycle(double *xw, double *bw, const doub
         __syncwarp();
         coarse_sweep3<L, LSH, FAST>(xw, bw, cf, false, lane);
     } else {
-        if (lane == 0) xw[0] = add_mul(0.0, coef[1 * kCoefStride + kCoarse], bw[0]);  // 1x1 solve
+        if (lane == 0)                                  // 1x1 solve
+            xw[Lc<1>::off] = add_mul(0.0, coef[1 * kCoefStride + kCoarse], bw[Lc<1>::off]);
         __syncwarp();
     }
 }
@@ -670,6 +669,8 @@ __device__ __forceinline__ void coarse_row(const MgCoarseArgs &a, double *xw, in
     const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
     const double *Bg = a.B + row * a.ldB;
     double *Xg = a.X + row * a.ldX;
+    for (int k = lane; k < kCoarseWords; k += 32) xw[k] = 0.0;   // pads stay zero
+    __syncwarp();
     for (int k = lane; k < m * m; k += 32) {
         const int q = Lc<TOP>::off + (k / m) * p + k % m;
         bw[q] = Bg[k];
