@@ -1105,7 +1105,8 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
     // large problems: copy f-hat in row chunks on a second stream and start
     // the (row-local) initial K_X on each chunk as it lands
     StagedInput staged;
-    const int64_t chunk_rows = 256;
+    // >= 256 rows per chunk (a one-wave K_X batch at least) and <= 8 chunks
+    const int64_t chunk_rows = std::max<int64_t>(256, (c->nt + 7) / 8);
     if (!c->domain && c->N >= (int64_t)1 << 26 && c->nt > chunk_rows) {
         if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         const int n = (int)((c->nt + chunk_rows - 1) / chunk_rows);
