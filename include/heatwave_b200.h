@@ -194,6 +194,10 @@ int hwg_pcg(hwg_ctx *ctx, const double *fhat, double *w, double epsilon, double 
 /*
  * End-to-end call for host buffers (the e2e leg of bench.py): copies fhat
  * from host memory, solves with hwg_pcg, applies u = W w and copies u back.
+ * For large problems (N >= 2^26) fhat is copied in up to 8 row chunks on a
+ * context-owned stream and the row-local initial K_X starts on each chunk as
+ * it lands (pinned host memory makes the copies asynchronous); results are
+ * bit-identical to hwg_pcg followed by W.
  */
 int hwg_solve_host(hwg_ctx *ctx, const double *fhat_host, double *u_host, double epsilon,
                    double rtol, int32_t max_iterations, int32_t recompute_every,
