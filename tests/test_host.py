@@ -196,3 +196,22 @@ def test_lshape_host_setup_matches_oracle():
     r = int(np.nonzero(np.all(np.rint(lv4.verts[lv4.interior] * 16) == [4, 4], axis=1))[0][0])
     assert sorted(Ao.tocsr()[r].data.tolist()) == sorted([A["c0"]] + [A["cx"]] * 2 + [A["cy"]] * 2)
     assert inputs.CONFIGS[5]["domain"] == "L"
+
+
+def test_bench_config5_workload_and_dof_bytes():
+    """bench.py --config 5: the per-GPU share of the 8-GPU L-shaped problem
+    (J = 8 + log2 N, mapped K = 11, D = I/4), with the algorithmic bytes
+    counted on the L's dofs (3/4 of the embedded grid)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    d, J, K, dist, u0, n_t, n_x = bench.workload(5)
+    assert (d, J, K, dist, n_t, n_x) == (2, 8, 11, "lshape", 257, 3141633)
+    assert bench.workload(5, 8)[1] == 11                # the full cfg 5 on 8 GPUs
+    assert bench.domain_of(5) == "L" and bench.domain_of(4) == "square"
+    assert np.array_equal(bench.diffusion_of(5, 2), 0.25 * np.eye(2))
+    frac = bench.dof_fraction(5, 2, 11, n_x)
+    assert abs(frac - 3141633 / 2047 ** 2) < 1e-15 and 0.74 < frac < 0.76
+    assert bench.dof_fraction(4, 2, 10, 1023 ** 2) == 1.0
+    assert "per-GPU share" in bench.workload_label(5, d, J, K, n_t, n_x)
