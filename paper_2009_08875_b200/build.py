@@ -44,8 +44,20 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def _compile(src):
+def _obj_fresh(src, obj):
+    """An object is reusable when it is newer than its source and every
+    shared header (incremental builds; build(force=True) ignores this)."""
+    if not os.path.exists(obj):
+        return False
+    t = os.path.getmtime(obj)
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
+    return all(os.path.getmtime(p) <= t for p in [src, *hdrs])
+
+
+def _compile(src, force=True):
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    if not force and _obj_fresh(src, obj):
+        return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -59,7 +71,7 @@ def build(force=False, verbose=False):
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(_compile, _sources()))
+        objs = list(ex.map(lambda s: _compile(s, force), _sources()))
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -88,7 +88,8 @@ struct hwg_ctx {
     cudaGraphExec_t graph_exec = nullptr; // one iteration (no recomputation) for graph_w
     cudaStream_t capture_stream = nullptr;  // graphs are captured here (the caller's stream
                                             // may be the legacy default stream)
-    const double *graph_w = nullptr;
+    const double *graph_w = nullptr;     // the graph bakes in w and the Schur form
+    int graph_form = -1;
     int64_t graph_kernels = 0;
     std::vector<cudaEvent_t> copy_events;
     int64_t bytes = 0;
@@ -101,6 +102,18 @@ struct hwg_ctx {
     std::vector<cudaEvent_t> prof_pool;
     double prof_ms[6] = {0}, prof_bytes[6] = {0};
     int64_t prof_n[6] = {0};
+};
+
+// Every entry point runs on its context's device and restores the caller's
+// current device on return (contexts on several GPUs in one process).
+struct DeviceGuard {
+    int prev = -1;
+    bool set = false;
+    explicit DeviceGuard(const hwg_ctx *c);
+    ~DeviceGuard()
+    {
+        if (set) cudaSetDevice(prev);
+    }
 };
 
 static cudaEvent_t prof_event(hwg_ctx *c)
@@ -154,6 +167,12 @@ struct ProfScope {
         }
     }
 };
+
+DeviceGuard::DeviceGuard(const hwg_ctx *c)
+{
+    if (!c || cudaGetDevice(&prev) != cudaSuccess) return;
+    if (prev != c->d.device && cudaSetDevice(c->d.device) == cudaSuccess) set = true;
+}
 
 static int dalloc(hwg_ctx *c, double **p, int64_t count)
 {
@@ -535,6 +554,14 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     if (d.vcycles < 1) return fail(HWG_EINVAL, "vcycles must be >= 1");
     if (!d.coef || !d.stencil_M || !d.stencil_A || !d.temporal || !d.wavelet_scale)
         return fail(HWG_EINVAL, "missing table in descriptor");
+    struct Restore {                      // leave the caller's current device as it was
+        int prev = -1;
+        Restore() { cudaGetDevice(&prev); }
+        ~Restore()
+        {
+            if (prev >= 0) cudaSetDevice(prev);
+        }
+    } restore_;
     CK(cudaSetDevice(d.device));
     hwg_ctx *c = new hwg_ctx();
     c->d = d;
@@ -643,6 +670,7 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
 
 int hwg_profile_enable(hwg_ctx *c, int enable)
 {
+    DeviceGuard dg_(c);
     if (!c) return fail(HWG_EINVAL, "null context");
     prof_flush(c);
     for (int k = 0; k < 6; ++k) {
@@ -655,6 +683,7 @@ int hwg_profile_enable(hwg_ctx *c, int enable)
 
 int hwg_profile_read(hwg_ctx *c, int kclass, double *ms, double *bytes, int64_t *launches)
 {
+    DeviceGuard dg_(c);
     if (!c || kclass < 0 || kclass >= 6) return fail(HWG_EINVAL, "bad profile class");
     prof_flush(c);
     if (ms) *ms = c->prof_ms[kclass];
@@ -665,6 +694,7 @@ int hwg_profile_read(hwg_ctx *c, int kclass, double *ms, double *bytes, int64_t 
 
 int hwg_destroy(hwg_ctx *c)
 {
+    DeviceGuard dg_(c);
     if (!c) return HWG_OK;
     prof_flush(c);
     for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
@@ -683,6 +713,7 @@ int64_t hwg_launch_count(const hwg_ctx *c) { return c ? c->launches : 0; }
 
 int hwg_wavelet(hwg_ctx *c, const double *X, double *Y, int transpose, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (X == Y) return fail(HWG_EINVAL, "wavelet input and output may not alias");
@@ -692,6 +723,7 @@ int hwg_wavelet(hwg_ctx *c, const double *X, double *Y, int transpose, void *str
 
 int hwg_spatial(hwg_ctx *c, int which, const double *X, double *Y, int64_t rows, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
     cudaStream_t st = S(stream);
     if (!c->domain || c->kernel_only) {          // kernel contexts: grid layout
@@ -713,6 +745,7 @@ int hwg_spatial(hwg_ctx *c, int which, const double *X, double *Y, int64_t rows,
 
 int hwg_schur_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (!c->domain) return schur(c, X, Y, S(stream));
@@ -723,6 +756,7 @@ int hwg_schur_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 
 int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (X == Y) return fail(HWG_EINVAL, "K_X input and output may not alias");
@@ -734,13 +768,20 @@ int hwg_kx_apply(hwg_ctx *c, const double *X, double *Y, void *stream)
 
 int hwg_set_schur_form(hwg_ctx *c, int form)
 {
+    DeviceGuard dg_(c);
     if (!c || (form != 0 && form != 1)) return fail(HWG_EINVAL, "form must be 0 (five-term) or 1 (test-space)");
+    if (form != c->form && c->graph_exec) {   // the captured iteration applies the old form
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+        c->graph_w = nullptr;
+    }
     c->form = form;
     return HWG_OK;
 }
 
 int hwg_grid_scatter(hwg_ctx *c, const double *X, double *Y, int64_t rows, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (X == Y && c->domain) return fail(HWG_EINVAL, "layout conversion may not alias");
     return to_grid(c, X, Y, rows, S(stream));
@@ -748,6 +789,7 @@ int hwg_grid_scatter(hwg_ctx *c, const double *X, double *Y, int64_t rows, void 
 
 int hwg_grid_gather(hwg_ctx *c, const double *X, double *Y, int64_t rows, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (X == Y && c->domain) return fail(HWG_EINVAL, "layout conversion may not alias");
     return from_grid(c, X, Y, rows, S(stream));
@@ -756,6 +798,7 @@ int hwg_grid_gather(hwg_ctx *c, const double *X, double *Y, int64_t rows, void *
 int hwg_mg_rows(hwg_ctx *c, int32_t op, const int32_t *op_host, const double *B, double *X,
                 int64_t rows, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !B || !X || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
     if (op < 0 || op > c->J + 1) return fail(HWG_EKEY, "no multigrid operator " + std::to_string(op));
@@ -785,6 +828,7 @@ int hwg_mg_rows(hwg_ctx *c, int32_t op, const int32_t *op_host, const double *B,
 int hwg_rhs(hwg_ctx *c, const double *F, const double *load, const double *u0proj,
             double *fhat, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !fhat) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     cudaStream_t st = S(stream);
@@ -835,6 +879,7 @@ int hwg_rhs(hwg_ctx *c, const double *F, const double *load, const double *u0pro
 int hwg_dot(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *result_host,
             void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || !result_host || rows < 0 || rows > c->rows_max)
         return fail(HWG_EINVAL, "bad argument");
     cudaStream_t st = S(stream);
@@ -876,7 +921,7 @@ static int enqueue_iteration(hwg_ctx *c, double *w, cudaStream_t st)
 // ~300 dependent launches become one graph launch
 static int iteration_graph(hwg_ctx *c, double *w)
 {
-    if (c->graph_exec && c->graph_w == w) return HWG_OK;
+    if (c->graph_exec && c->graph_w == w && c->graph_form == c->form) return HWG_OK;
     if (c->graph_exec) {
         cudaGraphExecDestroy(c->graph_exec);
         c->graph_exec = nullptr;
@@ -899,6 +944,7 @@ static int iteration_graph(hwg_ctx *c, double *w)
     cudaGraphDestroy(g);
     CK(ei);
     c->graph_w = w;
+    c->graph_form = c->form;
     c->graph_kernels = kernels;
     return HWG_OK;
 }
@@ -1072,6 +1118,7 @@ extern "C" {
 int hwg_pcg(hwg_ctx *c, const double *f, double *w, double epsilon, double rtol,
             int32_t max_iterations, int32_t recompute_every, hwg_pcg_stats *st_out, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !f || !w) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     if (!(epsilon > 0) && !(rtol > 0)) return fail(HWG_EINVAL, "tolerance must be positive");
@@ -1093,6 +1140,7 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
                    double rtol, int32_t max_iterations, int32_t recompute_every,
                    hwg_pcg_stats *stats, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !fhat_host || !u_host) return fail(HWG_EINVAL, "null argument");
     if (c->kernel_only) return fail(HWG_EINVAL, "kernel-only (distributed) context");
     cudaStream_t st = S(stream);
@@ -1152,6 +1200,7 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
 int hwg_syn_stage(hwg_ctx *c, int j, const double *C, int64_t c0, const double *Dw, int64_t d0,
                   double *Y, int64_t f0, int64_t nf, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !C || !Dw || !Y || j < 1 || j > c->J || nf < 0) return fail(HWG_EINVAL, "bad argument");
     CK(launch_syn_stage(j, c->scale[j - 1], C, c0, Dw, d0, Y, f0, nf, c->nx, S(stream)));
     ++c->launches;
@@ -1161,6 +1210,7 @@ int hwg_syn_stage(hwg_ctx *c, int j, const double *C, int64_t c0, const double *
 int hwg_ana_stage(hwg_ctx *c, int j, const double *X, int64_t x0, double *C, int64_t c0,
                   int64_t nc, double *Dw, int64_t d0, int64_t nd, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || (nc && !C) || (nd && !Dw) || j < 1 || j > c->J || nc < 0 || nd < 0)
         return fail(HWG_EINVAL, "bad argument");
     CK(launch_ana_stage(j, c->scale[j - 1], X, x0, C, c0, nc, Dw, d0, nd, c->nx, S(stream)));
@@ -1171,6 +1221,7 @@ int hwg_ana_stage(hwg_ctx *c, int j, const double *X, int64_t x0, double *C, int
 int hwg_bside_rows(hwg_ctx *c, const double *U, int64_t u0, int64_t nu, double *T1, double *T2,
                    int64_t r0, int64_t nr, double *E0, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !U || !T1 || !T2 || nr < 0 || r0 < 0 || r0 + nr > c->nt) return fail(HWG_EINVAL, "bad argument");
     if (u0 > (r0 > 0 ? r0 - 1 : 0) || u0 + nu < (r0 + nr < c->nt ? r0 + nr + 1 : r0 + nr))
         return fail(HWG_EINVAL, "U does not cover the rows the temporal bands need");
@@ -1185,6 +1236,7 @@ int hwg_bside_rows(hwg_ctx *c, const double *U, int64_t u0, int64_t nu, double *
 int hwg_bt_rows(hwg_ctx *c, const double *G1, const double *G2, const double *E0, double *out,
                 int64_t rows, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !G1 || !G2 || !out || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (rows == 0) return HWG_OK;
     CK(launch_bt_side(G1, G2, E0, out, c->grid, c->SM, c->SA, rows, S(stream)));
@@ -1195,6 +1247,7 @@ int hwg_bt_rows(hwg_ctx *c, const double *G1, const double *G2, const double *E0
 int hwg_mg_rows_dev(hwg_ctx *c, const int32_t *ops, const double *B, double *X, int64_t rows,
                     void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !ops || !B || !X || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
     if (rows == 0) return HWG_OK;
@@ -1204,6 +1257,7 @@ int hwg_mg_rows_dev(hwg_ctx *c, const int32_t *ops, const double *B, double *X, 
 int hwg_mg_rows_dev_dot(hwg_ctx *c, const int32_t *ops, const double *B, double *X, int64_t rows,
                         const double *Y, double *part, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !ops || !B || !X || !Y || !part || rows < 0) return fail(HWG_EINVAL, "bad argument");
     if (B == X) return fail(HWG_EINVAL, "MG input and output may not alias");
     if (rows == 0) return HWG_OK;
@@ -1213,6 +1267,7 @@ int hwg_mg_rows_dev_dot(hwg_ctx *c, const int32_t *ops, const double *B, double 
 int hwg_row_partials(hwg_ctx *c, const double *X, const double *Y, int64_t rows, double *part,
                      void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || !part || rows < 0) return fail(HWG_EINVAL, "bad argument");
     CK(launch_row_partials(X, Y, rows, c->nx, part, S(stream)));
     ++c->launches;
@@ -1221,6 +1276,7 @@ int hwg_row_partials(hwg_ctx *c, const double *X, const double *Y, int64_t rows,
 
 int hwg_tree_sum(hwg_ctx *c, const double *part, int64_t n, double *result, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !part || !result || n < 0 || n + 4 > c->red_max) return fail(HWG_EINVAL, "bad argument");
     CK(launch_tree(part, n, c->tmp, result, S(stream)));
     ++c->launches;
@@ -1229,6 +1285,7 @@ int hwg_tree_sum(hwg_ctx *c, const double *part, int64_t n, double *result, void
 
 int hwg_axpy(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || n < 0) return fail(HWG_EINVAL, "bad argument");
     CK(launch_axpy(a, X, Y, n, S(stream)));
     ++c->launches;
@@ -1237,6 +1294,7 @@ int hwg_axpy(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *
 
 int hwg_xpay(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || n < 0) return fail(HWG_EINVAL, "bad argument");
     CK(launch_xpay(a, X, Y, n, S(stream)));
     ++c->launches;
@@ -1246,6 +1304,7 @@ int hwg_xpay(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *
 int hwg_temporal_rows(hwg_ctx *c, int band, const double *X, int64_t x0, double *Y, int64_t r0,
                       int64_t nr, void *stream)
 {
+    DeviceGuard dg_(c);
     if (!c || !X || !Y || nr < 0 || r0 < 0) return fail(HWG_EINVAL, "bad argument");
     const DevBand *bands[8] = {&c->Mt, &c->At, &c->L, &c->LT, &c->T, &c->TT, &c->Nn, &c->NT};
     if (band < 0 || band > 7) return fail(HWG_EINVAL, "unknown temporal band");

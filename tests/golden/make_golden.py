@@ -135,7 +135,7 @@ LEAN_DROP = ("load", "ky", "g_ss", "g_hat", "u0_hat", "MxP", "AxP", "WP")
 
 
 def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.0,
-             domain="square", u0=None):
+             domain="square", u0=None, nsample=4096):
     t0 = time.time()
     problem = problem_for(d, dist, D, c, u0)
     asm = assemble_reference(problem, J, K, domain)
@@ -168,10 +168,13 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.
                 stencils=stencil_table(asm, problem))
     arrays = dict(u0proj=u0proj)
     rng = np.random.default_rng(PROBE_SEED)
-    idx = np.sort(rng.choice(n_t * n_x, size=min(4096, n_t * n_x), replace=False))
+    idx = np.sort(rng.choice(n_t * n_x, size=min(nsample, n_t * n_x), replace=False))
     arrays["sample_idx"] = idx
     arrays["u_sample"] = u.reshape(-1)[idx]
     arrays["fhat_sample"] = fhat.reshape(-1)[idx]
+    if nsample > 4096:                   # large twins: also w, and u's final-time row norm
+        arrays["w_sample"] = res.w.array.reshape(-1)[idx]
+        meta["u_last_row_norm"] = float(np.linalg.norm(u[-1]))
     if full:
         P = np.random.default_rng(PROBE_SEED).standard_normal((n_t, n_x))
         arrays.update(fhat=fhat, load=y, ky=ky, g_ss=g_ss, g_hat=g_hat,
@@ -206,9 +209,11 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.
           f"{meta['seconds']:.1f}s", flush=True)
 
 
-def mg_rows_case(name, d, K, rows=1, domain="square", D=None):
+def mg_rows_case(name, d, K, rows=1, domain="square", D=None, nsample=0):
     """Full outputs of K_x (alpha=1, mu=0) and C_j (alpha=0.3, mu=2^j) MG
-    applies on seeded rows at a larger K (streaming-kernel sizes)."""
+    applies on seeded rows at a larger K (streaming-kernel sizes).
+    ``nsample`` > 0: store only that many seeded sample positions per row
+    plus the row norms (K = 10 rows are 8.4 MB each)."""
     hier = hw.build_mesh_hierarchy(d, K) if domain == "square" else lshape_hierarchy(K)
     ops = hw.assemble_level_operators(hier, D)
     n = ops[-1].A_x.rows
@@ -222,7 +227,13 @@ def mg_rows_case(name, d, K, rows=1, domain="square", D=None):
         X = np.empty_like(B)
         mg.apply_rows(B, X, 0, rows)
         key = f"a{alpha:g}_mu{mu:g}"
-        arrays[key] = X
+        if nsample:
+            idx = np.sort(np.random.default_rng(PROBE_SEED + 1).choice(n, nsample, replace=False))
+            arrays["sample_idx"] = idx
+            arrays[key] = X[:, idx]
+            meta.setdefault("row_norms", {})[key] = np.linalg.norm(X, axis=1).tolist()
+        else:
+            arrays[key] = X
         meta["solvers"].append(dict(key=key, alpha=alpha, mu=mu))
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
     with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
@@ -330,6 +341,17 @@ CASES = {
     "mg8": lambda: mg_rows_case("mg8", 2, 8),
     "mg1d10": lambda: mg_rows_case("mg1d10", 1, 10, rows=4),
     "wav10": lambda: wavelet_case("wav10", 10, 3),
+    # round 2: pins at the benched configs' shapes (the reference cannot hold
+    # cfg 3/4 in this container's 62 GB: SURVEY §7 "oracle reach")
+    # K = 10 MG rows: the n = 1023 finest-level kernels cfg 4 runs
+    "mg10": lambda: mg_rows_case("mg10", 2, 10, rows=2, nsample=65536),
+    # J = 4, K = 10: a full PCG through every cfg 4 kernel variant (5-point
+    # K_x batch, zero-start DOWN, fused r.z UP at n = 1023)
+    "c410": lambda: run_case("c410", 2, 4, 10, "uniform", full=False, nsample=65536),
+    # J = 10 (cfg 4's N_t and wavelet levels), K = 8
+    "t10k8": lambda: run_case("t10k8", 2, 10, 8, "uniform", full=False, nsample=65536),
+    # 1D J = 16, K = 10 (cfg 3's N_x, 65,537 temporal rows)
+    "d16": lambda: run_case("d16", 1, 16, 10, "normal", full=False, nsample=65536),
     "load": check_interpolant_load,
 }
 
