@@ -201,6 +201,19 @@ def workload_label(cfg, d, J, K, n_t, n_x, world=1):
     return (f"cfg{cfg}: {d}D heat, J={J} (N_t={n_t}), K={K} (N_x={n_x}), PCG to rtol 1e-6")
 
 
+def config_dict(cfg, world=1, slab=False):
+    """The `config` object of the JSON line -- identical for both arms (the
+    reference arm times a bounded sample of this workload, described in its
+    cpu_baseline.sample)."""
+    d, J, K, dist, u0, n_t, n_x = workload(cfg, world)
+    par = "1 GPU" if world == 1 and not slab else (
+        f"time slabs x{world} (NCCL halos + allgather)" if world > 1 or slab else "1 GPU")
+    return {"workload": workload_label(cfg, d, J, K, n_t, n_x, world), "dofs": n_t * n_x,
+            "parallelism": par,
+            "l2": "inputs larger than L2 (each solve streams >100 arrays of "
+                  f"{8 * n_t * n_x / 1e6:.0f} MB)"}
+
+
 # --------------------------------------------------------------------------
 # CPU oracle legs (cpu_baseline and --impl reference)
 # --------------------------------------------------------------------------
@@ -263,11 +276,16 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE recipe)",
-        "config": {"workload": f"cfg{args.config}", "sample": label, "d": d, "J": J, "K": K},
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.config == 5 else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded BASELINE cfg{args.config} recipe)",
+        "config": config_dict(args.config, max(args.gpus, 1)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} PCG iterations, {label}, oracle/ C+OpenMP"},
+                         "sample": f"one step = one PCG iteration of the oracle (oracle/ C+OpenMP, "
+                                   f"{threads} threads) on a bounded sample of the workload: "
+                                   f"{label} (throughput per DoF is flat in N_t, SURVEY §8d); "
+                                   f"{args.steps} timed steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -288,8 +306,15 @@ def run_ours(args):
     N = n_t * n_x
     problem = hw.ProblemData(D=diffusion_of(args.config, d), c=0.0, u0=u0)
     F = inputs.forcing(dist_name, n_t, n_x)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     asm = hw.assemble_system(problem, J, K, hw.SolveConfig(device=local), forcing=F,
                              host_rhs=False, domain=domain_of(args.config))
+    torch.cuda.synchronize()
+    # assemble_system (solver.py:353-386): context, tables, workspaces, and the
+    # GPU right-hand side from the host forcing array (its H2D copy included)
+    setup_s = {"assemble_system": time.perf_counter() - t_setup,
+               "includes": "ctx/tables/workspaces + H2D of the nodal forcing + GPU f-hat"}
     del F
     ctx = asm.ctx
     f = asm.rhs.f_hat.array
@@ -397,12 +422,10 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (seeded BASELINE cfg{args.config} recipe: {dist_name} nodal "
                     "forcing, blockwise-seeded)",
-            "config": {"workload": workload_label(args.config, d, J, K, n_t, n_x),
-                       "dofs": N, "iterations_per_solve": its_list[0],
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 (each solve streams >100 arrays of "
-                             f"{8 * N / 1e6:.0f} MB)"},
+            "config": config_dict(args.config, world),
+            "iterations_per_solve": its_list[0],
             "time_to_solve_s": ms_max / 1e3 / args.steps,
+            "setup_s": setup_s,
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "launches": dn, "bytes_per_launch": dbytes / max(dn, 1),
@@ -451,6 +474,8 @@ def run_slab(args):
     d, J, K, dist_name, u0, n_t, n_x = workload(args.config, world)
     N = n_t * n_x
     domain = domain_of(args.config)
+    torch.cuda.synchronize()
+    t_setup0 = time.perf_counter()
     states = D.make_states(d, J, K, world, [rank], lambda p: dev, D=diffusion_of(args.config, d),
                            domain=domain)
     system = D.SlabSystem(states, D.TorchComm())
@@ -460,8 +485,14 @@ def run_slab(args):
     def frows(a, b):
         return torch.from_numpy(inputs.forcing_rows(dist_name, n_t, n_x, a, b)).to(dev)
 
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     u0p = torch.from_numpy(disc.project_initial(disc.FineMesh(d, K, domain), u0)).to(dev)
     F = D.rhs(system, frows, u0p)
+    torch.cuda.synchronize()
+    setup_s = {"assemble_system": time.perf_counter() - t_setup0, "rhs": time.perf_counter() - t_setup,
+               "includes": "rank contexts + forcing rows generated on the host + H2D + "
+                           "distributed GPU f-hat"}
     W = [torch.empty_like(F[0])]
 
     def solve():
@@ -525,11 +556,10 @@ def run_slab(args):
             "higher_is_better": True, "scaling": "weak" if args.config == 5 else "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE recipe, blockwise-seeded forcing rows)",
-            "config": {"workload": workload_label(args.config, d, J, K, n_t, n_x, world),
-                       "dofs": N, "iterations_per_solve": its_list[0],
-                       "parallelism": f"time slabs x{world} (NCCL halos + allgather)",
-                       "l2": "inputs larger than L2"},
+            "config": config_dict(args.config, world, slab=True),
+            "iterations_per_solve": its_list[0],
             "time_to_solve_s": ms_max / 1e3 / args.steps,
+            "setup_s": setup_s,
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                          "launches": dn, "bytes_per_launch": dbytes / max(dn, 1),
@@ -558,6 +588,20 @@ def run_slab(args):
     return 0
 
 
+def launcher_command(argv, n, port):
+    """torchrun command that re-runs this script as n ranks (one per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__), *argv]
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -569,9 +613,24 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slab", action="store_true", help="time-slab path even at N = 1")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0")) or None
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
-        return run_reference(args)
-    if args.slab or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_reference(args)            # rank 0 only; other ranks exit 0
+    if world is None and args.gpus > 1:
+        # one process per GPU: re-launch this script under torchrun
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) "
+                  "are visible", file=sys.stderr)
+            return 2
+        return subprocess.call(launcher_command(sys.argv[1:], args.gpus, _free_port()))
+    if world is not None and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.slab or (world or 1) > 1:
         return run_slab(args)
     return run_ours(args)
 

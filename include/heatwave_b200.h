@@ -229,9 +229,11 @@ int hwg_profile_read(hwg_ctx *ctx, int kclass, double *ms, double *bytes, int64_
 
 /* Synthesis stage j (wavelet.py:114-137 with M_j of :56-76): Y[f - f0] for
  * fine nodes f in [f0, f0 + nf) from coarse nodal rows C (C[i - c0] = node
- * i of level j-1) and level-j wavelet rows Dw (Dw[k - d0] = wavelet k). */
+ * i of level j-1) and level-j wavelet rows Dw (Dw[k - d0] = wavelet k).
+ * Dhalo (nullable): wavelet d0 - 1 (a neighbour slab's halo row), so the
+ * caller's own rows are read in place. */
 int hwg_syn_stage(hwg_ctx *ctx, int j, const double *C, int64_t c0, const double *Dw, int64_t d0,
-                  double *Y, int64_t f0, int64_t nf, void *stream);
+                  const double *Dhalo, double *Y, int64_t f0, int64_t nf, void *stream);
 
 /* Transposed stage j: C[i - c0] = (P_j^T x)[i] for i in [c0, c0 + nc) and
  * Dw[k - d0] = (Q_j^T x)[k] for k in [d0, d0 + nd), from fine nodal rows X
@@ -286,6 +288,28 @@ int hwg_tree_sum(hwg_ctx *ctx, const double *part, int64_t n, double *result, vo
  * _kernels.py:64-76). */
 int hwg_axpy(hwg_ctx *ctx, double a, const double *X, double *Y, int64_t n, void *stream);
 int hwg_xpay(hwg_ctx *ctx, double a, const double *X, double *Y, int64_t n, void *stream);
+
+/* Device-resident PCG scalars for the time-slab solver (solver.py:212-256),
+ * the same kernels hwg_pcg runs.  scal (device, >= 5 doubles): [0] rho,
+ * [1] p.q, [2] rho_new, [3] alpha, [4] beta.  step 0: alpha = rho / pq;
+ * step 1: beta = rho_new / rho, rho = rho_new. */
+int hwg_pcg_scalar(hwg_ctx *ctx, int step, double *scal, void *stream);
+
+/* w += alpha p (if do_w); r -= alpha q (if do_r); alpha = scal[3]. */
+int hwg_pcg_update_wr(hwg_ctx *ctx, double *w, double *r, const double *p, const double *q,
+                      const double *scal, int64_t n, int do_w, int do_r, void *stream);
+
+/* w += alpha p (if do_w, the deferred half of the step above) and
+ * p = z + beta p in one pass over p; alpha = scal[3], beta = scal[4]. */
+int hwg_pcg_update_wp(hwg_ctx *ctx, double *w, double *p, const double *z, const double *scal,
+                      int64_t n, int do_w, void *stream);
+
+/* r = f - t (the periodic residual recomputation, solver.py:227-229). */
+int hwg_sub(hwg_ctx *ctx, const double *f, const double *t, double *r, int64_t n, void *stream);
+
+/* *flag (device int) |= any(X[0:n] != 0)  (the zero right-hand side test,
+ * solver.py:196-198; the caller zeroes *flag). */
+int hwg_any_nonzero(hwg_ctx *ctx, const double *X, int64_t n, int32_t *flag, void *stream);
 
 #ifdef __cplusplus
 }

@@ -26,7 +26,9 @@ EXPORTS = ("hwg_last_error", "hwg_version", "hwg_create", "hwg_destroy",
            "hwg_solve_host", "hwg_launch_count", "hwg_profile_enable", "hwg_profile_read",
            "hwg_syn_stage", "hwg_ana_stage", "hwg_bside_rows", "hwg_bt_rows", "hwg_mg_rows_dev",
            "hwg_mg_rows_dev_dot", "hwg_grid_scatter", "hwg_grid_gather", "hwg_set_schur_form",
-           "hwg_row_partials", "hwg_tree_sum", "hwg_axpy", "hwg_xpay", "hwg_temporal_rows")
+           "hwg_row_partials", "hwg_tree_sum", "hwg_axpy", "hwg_xpay", "hwg_temporal_rows",
+           "hwg_pcg_scalar", "hwg_pcg_update_wr", "hwg_pcg_update_wp", "hwg_sub",
+           "hwg_any_nonzero")
 
 _P = C.c_void_p
 _D = C.c_double
@@ -99,7 +101,7 @@ def _bind(L):
     L.hwg_pcg.argtypes = [_P, _P, _P, _D, _D, _I32, _I32, C.POINTER(HwgPcgStats), _P]
     L.hwg_profile_enable.argtypes = [_P, C.c_int]
     L.hwg_profile_read.argtypes = [_P, C.c_int, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64)]
-    L.hwg_syn_stage.argtypes = [_P, C.c_int, _P, _I64, _P, _I64, _P, _I64, _I64, _P]
+    L.hwg_syn_stage.argtypes = [_P, C.c_int, _P, _I64, _P, _I64, _P, _P, _I64, _I64, _P]
     L.hwg_ana_stage.argtypes = [_P, C.c_int, _P, _I64, _P, _I64, _I64, _P, _I64, _I64, _P]
     L.hwg_bside_rows.argtypes = [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _P, _P]
     L.hwg_bt_rows.argtypes = [_P, _P, _P, _P, _P, _I64, _P]
@@ -113,6 +115,11 @@ def _bind(L):
     L.hwg_axpy.argtypes = [_P, _D, _P, _P, _I64, _P]
     L.hwg_xpay.argtypes = [_P, _D, _P, _P, _I64, _P]
     L.hwg_temporal_rows.argtypes = [_P, C.c_int, _P, _I64, _P, _I64, _I64, _P]
+    L.hwg_pcg_scalar.argtypes = [_P, C.c_int, _P, _P]
+    L.hwg_pcg_update_wr.argtypes = [_P, _P, _P, _P, _P, _P, _I64, C.c_int, C.c_int, _P]
+    L.hwg_pcg_update_wp.argtypes = [_P, _P, _P, _P, _P, _I64, C.c_int, _P]
+    L.hwg_sub.argtypes = [_P, _P, _P, _P, _I64, _P]
+    L.hwg_any_nonzero.argtypes = [_P, _P, _I64, _P, _P]
     L.hwg_solve_host.argtypes = [_P, _P, _P, _D, _D, _I32, _I32, C.POINTER(HwgPcgStats), _P]
     for name in EXPORTS:
         if name not in ("hwg_last_error", "hwg_version", "hwg_workspace_bytes",

@@ -1198,11 +1198,11 @@ int hwg_solve_host(hwg_ctx *c, const double *fhat_host, double *u_host, double e
 
 // ---- time-slab building blocks --------------------------------------------
 int hwg_syn_stage(hwg_ctx *c, int j, const double *C, int64_t c0, const double *Dw, int64_t d0,
-                  double *Y, int64_t f0, int64_t nf, void *stream)
+                  const double *Dhalo, double *Y, int64_t f0, int64_t nf, void *stream)
 {
     DeviceGuard dg_(c);
     if (!c || !C || !Dw || !Y || j < 1 || j > c->J || nf < 0) return fail(HWG_EINVAL, "bad argument");
-    CK(launch_syn_stage(j, c->scale[j - 1], C, c0, Dw, d0, Y, f0, nf, c->nx, S(stream)));
+    CK(launch_syn_stage(j, c->scale[j - 1], C, c0, Dw, d0, Dhalo, Y, f0, nf, c->nx, S(stream)));
     ++c->launches;
     return HWG_OK;
 }
@@ -1297,6 +1297,58 @@ int hwg_xpay(hwg_ctx *c, double a, const double *X, double *Y, int64_t n, void *
     DeviceGuard dg_(c);
     if (!c || !X || !Y || n < 0) return fail(HWG_EINVAL, "bad argument");
     CK(launch_xpay(a, X, Y, n, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_pcg_scalar(hwg_ctx *c, int step, double *scal, void *stream)
+{
+    DeviceGuard dg_(c);
+    if (!c || !scal || (step != 0 && step != 1)) return fail(HWG_EINVAL, "bad argument");
+    CK(step == 0 ? launch_pcg_alpha(scal, S(stream)) : launch_pcg_beta(scal, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_pcg_update_wr(hwg_ctx *c, double *w, double *r, const double *p, const double *q,
+                      const double *scal, int64_t n, int do_w, int do_r, void *stream)
+{
+    DeviceGuard dg_(c);
+    if (!c || !scal || n < 0 || (do_w && (!w || !p)) || (do_r && (!r || !q)))
+        return fail(HWG_EINVAL, "bad argument");
+    if (n == 0 || (!do_w && !do_r)) return HWG_OK;
+    CK(launch_update_wr(w, r, p, q, scal, n, do_w ? 1 : 0, do_r ? 1 : 0, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_pcg_update_wp(hwg_ctx *c, double *w, double *p, const double *z, const double *scal,
+                      int64_t n, int do_w, void *stream)
+{
+    DeviceGuard dg_(c);
+    if (!c || !p || !z || !scal || n < 0 || (do_w && !w)) return fail(HWG_EINVAL, "bad argument");
+    if (n == 0) return HWG_OK;
+    CK(launch_update_wp(w, p, z, scal, n, do_w ? 1 : 0, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_sub(hwg_ctx *c, const double *f, const double *t, double *r, int64_t n, void *stream)
+{
+    DeviceGuard dg_(c);
+    if (!c || !f || !t || !r || n < 0) return fail(HWG_EINVAL, "bad argument");
+    if (n == 0) return HWG_OK;
+    CK(launch_sub(f, t, r, n, S(stream)));
+    ++c->launches;
+    return HWG_OK;
+}
+
+int hwg_any_nonzero(hwg_ctx *c, const double *X, int64_t n, int32_t *flag, void *stream)
+{
+    DeviceGuard dg_(c);
+    if (!c || !X || !flag || n < 0) return fail(HWG_EINVAL, "bad argument");
+    if (n == 0) return HWG_OK;
+    CK(launch_any_nonzero(X, n, (int *)flag, S(stream)));
     ++c->launches;
     return HWG_OK;
 }

@@ -72,9 +72,10 @@ cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
 cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
                           const double *scale, int64_t nt, int64_t nx, bool transpose,
                           cudaStream_t st, int64_t *launches, int mask_n = 0, int mask_lm = 0);
+// Dh (nullable): wavelet row d0 - 1 held apart from Dm (a slab's halo row)
 cudaError_t launch_syn_stage(int j, double s, const double *C, int64_t c0, const double *Dm,
-                             int64_t d0, double *Y, int64_t f0, int64_t nf, int64_t nx,
-                             cudaStream_t st);
+                             int64_t d0, const double *Dh, double *Y, int64_t f0, int64_t nf,
+                             int64_t nx, cudaStream_t st);
 cudaError_t launch_ana_stage(int j, double s, const double *X, int64_t x0, double *C, int64_t c0,
                              int64_t nc, double *Dm, int64_t d0, int64_t nd, int64_t nx,
                              cudaStream_t st);

@@ -143,6 +143,7 @@ static dim3 pair_grid(int pairs, int64_t nx)
 // Y[f - f0] <- (M_j [c ; d])[f], f in [f0, f0 + nf); C[i - c0], Dm[k - d0]
 __global__ void __launch_bounds__(kWavBS) wav_syn_window(const double *__restrict__ C, int64_t c0,
                                                          const double *__restrict__ Dm, int64_t d0,
+                                                         const double *__restrict__ Dh,
                                                          double *__restrict__ Y, int64_t f0,
                                                          int64_t nf, int j, double s, int64_t nx)
 {
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kWavBS) wav_syn_window(const double *__restric
     const int64_t q0 = qlo + (int64_t)blockIdx.y * kWavQP;
     const int64_t q1 = q0 + kWavQP - 1 < qhi ? q0 + kWavQP - 1 : qhi;
     auto cr = [&](int64_t q) { return C[(q - c0) * nx + i]; };
-    auto dr = [&](int64_t k) { return Dm[(k - d0) * nx + i]; };
+    auto dr = [&](int64_t k) { return (Dh && k < d0) ? Dh[i] : Dm[(k - d0) * nx + i]; };
     double cq = 0.0, dm = 0.0;
     bool have_c = false, have_d = false;
     for (int64_t q = q0; q <= q1; ++q) {
@@ -235,12 +236,13 @@ __global__ void __launch_bounds__(kWavBS) wav_ana_window(const double *__restric
 }
 
 cudaError_t launch_syn_stage(int j, double s, const double *C, int64_t c0, const double *Dm,
-                             int64_t d0, double *Y, int64_t f0, int64_t nf, int64_t nx,
-                             cudaStream_t st)
+                             int64_t d0, const double *Dh, double *Y, int64_t f0, int64_t nf,
+                             int64_t nx, cudaStream_t st)
 {
     if (nf <= 0) return cudaSuccess;
     const int64_t pairs = ((f0 + nf - 1) >> 1) - (f0 >> 1) + 1;
-    wav_syn_window<<<pair_grid((int)pairs, nx), kWavBS, 0, st>>>(C, c0, Dm, d0, Y, f0, nf, j, s, nx);
+    wav_syn_window<<<pair_grid((int)pairs, nx), kWavBS, 0, st>>>(C, c0, Dm, d0, Dh, Y, f0, nf, j, s,
+                                                                 nx);
     return cudaGetLastError();
 }
 

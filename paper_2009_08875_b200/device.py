@@ -124,8 +124,9 @@ class GpuContext:
         return out
 
     # ---- time-slab building blocks (distributed path) ----------------------
-    def syn_stage(self, j, C, c0, Dw, d0, Y, f0, nf):
-        _lib.check(self.lib.hwg_syn_stage(self.handle, j, ptr(C), c0, ptr(Dw), d0, ptr(Y), f0, nf,
+    def syn_stage(self, j, C, c0, Dw, d0, Y, f0, nf, Dh=None):
+        _lib.check(self.lib.hwg_syn_stage(self.handle, j, ptr(C), c0, ptr(Dw), d0,
+                                          ptr(Dh) if Dh is not None else None, ptr(Y), f0, nf,
                                           self.stream()))
 
     def ana_stage(self, j, X, x0, C, c0, nc, Dw, d0, nd):
@@ -182,6 +183,26 @@ class GpuContext:
 
     def xpay(self, a, X, Y):
         _lib.check(self.lib.hwg_xpay(self.handle, float(a), ptr(X), ptr(Y), X.numel(), self.stream()))
+
+    # device-resident PCG scalars (scal: [rho, pq, rho_new, alpha, beta, ...])
+    def pcg_scalar(self, step, scal):
+        _lib.check(self.lib.hwg_pcg_scalar(self.handle, int(step), ptr(scal), self.stream()))
+
+    def pcg_update_wr(self, w, r, p, q, scal, do_w, do_r):
+        _lib.check(self.lib.hwg_pcg_update_wr(self.handle, ptr(w), ptr(r), ptr(p), ptr(q), ptr(scal),
+                                              p.numel(), int(do_w), int(do_r), self.stream()))
+
+    def pcg_update_wp(self, w, p, z, scal, do_w):
+        _lib.check(self.lib.hwg_pcg_update_wp(self.handle, ptr(w), ptr(p), ptr(z), ptr(scal),
+                                              p.numel(), int(do_w), self.stream()))
+
+    def sub(self, f, t, r):
+        _lib.check(self.lib.hwg_sub(self.handle, ptr(f), ptr(t), ptr(r), f.numel(), self.stream()))
+
+    def any_nonzero(self, X, flag):
+        """flag (int32 device tensor) |= any(X != 0)."""
+        _lib.check(self.lib.hwg_any_nonzero(self.handle, ptr(X), X.numel(), ptr(flag),
+                                            self.stream()))
 
     def wavelet(self, X, Y, transpose):
         _lib.check(self.lib.hwg_wavelet(self.handle, ptr(X), ptr(Y), int(transpose), self.stream()))

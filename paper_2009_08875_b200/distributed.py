@@ -169,6 +169,14 @@ class SimComm:
         stacked = torch.stack(list(tensors))
         return [stacked for _ in states]
 
+    def allreduce_max(self, tensors):
+        import torch
+        m = torch.stack(list(tensors)).amax(dim=0)
+        for t in tensors:
+            t.copy_(m)
+
+    capturable = True         # device copies only: a whole iteration fits one CUDA graph
+
 
 class TorchComm:
     """torch.distributed process group (NCCL between GPUs, gloo on CPUs)."""
@@ -199,9 +207,27 @@ class TorchComm:
     def allgather(self, states, tensors):
         import torch
         (t,) = tensors
-        out = [torch.empty_like(t) for _ in range(self.P)]
-        self.dist.all_gather(out, t.contiguous())
-        return [torch.stack(out)]
+        if self.P == 1:
+            return [t.unsqueeze(0)]
+        out = torch.empty((self.P, *t.shape), dtype=t.dtype, device=t.device)
+        if t.is_cuda:                        # NCCL: one gather into a flat buffer
+            self.dist.all_gather_into_tensor(out, t.contiguous())
+        else:                                # gloo has no flat all-gather
+            self.dist.all_gather(list(out.unbind(0)), t.contiguous())
+        return [out]
+
+    def allreduce_max(self, tensors):
+        (t,) = tensors
+        if self.P > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+
+    @property
+    def capturable(self):
+        # one rank: no collective at all.  P > 1: NCCL inside a captured graph
+        # is opt-in (HWG_SLAB_GRAPH=1); by default the iteration is issued
+        # eagerly, still with a single host synchronisation.
+        import os
+        return self.P == 1 or os.environ.get("HWG_SLAB_GRAPH") == "1"
 
 
 # --------------------------------------------------------------------------
@@ -219,7 +245,7 @@ class RankState:
         H = lay.H
         z = lambda r: torch.zeros((r, n_x), dtype=dtype, device=device)  # noqa: E731
         self.bufs = {"U": z(H + 2), "Xa": z(H + 2), "B1": z(H + 2), "B2": z(H + 2),
-                     "D": z(H // 2 + 2), "X": None}
+                     "D": z(1), "X": None}            # D: the left neighbour's wavelet halo row
         self.CN = [z(2 ** j + 1) for j in range(lay.L0 + 1)]     # replicated coarse nodal
         self.T12 = z(2 * lay.n_out)
         self.G12 = z(2 * lay.n_out)
@@ -243,6 +269,13 @@ class RankState:
         self.gdst = torch.as_tensor(np.concatenate(dst_idx), device=device)
         self.glob = torch.zeros(2 ** J + 1, dtype=dtype, device=device)
         self.res = torch.zeros(1, dtype=dtype, device=device)
+        self.contrib = torch.zeros(lay.n_w, dtype=dtype, device=device)
+        # PCG scalars on the device: [rho, pq, rho_new, alpha, beta] (hwg_pcg's
+        # layout) and their pinned host mirror, read once per iteration
+        self.scal = torch.zeros(8, dtype=dtype, device=device)
+        is_cuda = torch.device(device).type == "cuda"
+        self.hscal = torch.zeros(8, dtype=dtype, pin_memory=is_cuda)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
 
 
 # --------------------------------------------------------------------------
@@ -276,13 +309,10 @@ class SlabSystem:
                 cin = st.CN[L0][lay.p:lay.p + 2] if j == L0 + 1 else \
                     st.bufs[_syn_buf(j - 1, J)][1:n_c + 2]
                 off, n = lay.block[j]
-                D = st.bufs["D"]
-                if lay.p == 0:
-                    D[0].zero_()
-                D[1:1 + n].copy_(x[off:off + n])
+                halo = st.bufs["D"][0] if lay.p > 0 else None     # wavelet c0 - 1
                 out = st.bufs[_syn_buf(j, J)][1:]
-                st.k.syn_stage(j, cin, c0, D[:n + 1], c0 - 1, out, 2 * c0,
-                               2 * n_c + (1 if lay.last else 0))
+                st.k.syn_stage(j, cin, c0, x[off:off + n], c0, out, 2 * c0,
+                               2 * n_c + (1 if lay.last else 0), Dh=halo)
 
     # W^T: nodal rows in Xa[1 : 1 + n_out] -> wavelet Y
     def analysis(self, Y):
@@ -337,36 +367,87 @@ class SlabSystem:
             st.k.spatial(1, y, st.mid)
             st.k.mg_rows_dev(st.ops_kx, st.mid, y)
 
-    def kx_dot(self, X, Y):
-        """Y = K_X X and <X, Y>, the per-row partials fused into the last
-        multigrid pass (the same kernels as the single-GPU hwg_pcg)."""
+    def kx_dot_dev(self, X, Y, slot):
+        """Y = K_X X and <X, Y> -> scal[slot] on every rank's device, the
+        per-row partials fused into the last multigrid pass (the same kernels
+        as the single-GPU hwg_pcg)."""
         for st, x, y in zip(self.states, X, Y):
             st.k.mg_rows_dev(st.ops_kx, x, y)
             st.k.spatial(1, y, st.mid)
             st.k.mg_rows_dev_dot(st.ops_kx, st.mid, y, x, st.part)
-        return self._reduce_partials()
+        self._reduce_partials(slot)
 
-    def dot(self, X, Y):
-        """Inner product with the reference's fixed tree over the per-row
-        partials in GLOBAL row order (solver.py:111-129) -- identical for
-        every number of ranks."""
+    def dot_dev(self, X, Y, slot):
+        """<X, Y> -> scal[slot] (device) with the reference's fixed tree over
+        the per-row partials in GLOBAL row order (solver.py:111-129) --
+        identical for every number of ranks."""
         for st, x, y in zip(self.states, X, Y):
             st.k.row_partials(x, y, st.part)
-        return self._reduce_partials()
+        self._reduce_partials(slot)
 
-    def _reduce_partials(self):
-        contrib = []
+    def kx_dot(self, X, Y):
+        self.kx_dot_dev(X, Y, 5)
+        return self.read_scalar(5)
+
+    def dot(self, X, Y):
+        self.dot_dev(X, Y, 5)
+        return self.read_scalar(5)
+
+    def _reduce_partials(self, slot):
+        import torch
         for st in self.states:
-            contrib.append(st.part * st.owned)
-        gathered = self.comm.allgather(self.states, contrib)
-        vals = []
+            torch.mul(st.part, st.owned, out=st.contrib)
+        gathered = self.comm.allgather(self.states, [st.contrib for st in self.states])
         for st, g in zip(self.states, gathered):
             st.glob[st.gdst] = g.reshape(-1)[st.gsrc]
-            st.k.tree_sum(st.glob, st.glob.numel(), st.res)
-            vals.append(float(st.res.item()))
-        if len(set(vals)) != 1:
-            raise RuntimeError("ranks disagree on an inner product")
-        return vals[0]
+            st.k.tree_sum(st.glob, st.glob.numel(), st.scal[slot:slot + 1])
+
+    def read_scalar(self, slot):
+        """One scalar from rank-local device memory (a host synchronisation;
+        every rank holds the same value)."""
+        return float(self.states[0].scal[slot].item())
+
+    def read_scalars(self):
+        """The pinned mirror filled at the end of an iteration (one sync)."""
+        import torch
+        if self.states[0].scal.is_cuda:
+            torch.cuda.current_stream(self.states[0].scal.device).synchronize()
+        return self.states[0].hscal.tolist()
+
+    def any_nonzero(self, X):
+        """any(X != 0) over all ranks (the reference's zero right-hand side
+        test, np.any(f), solver.py:196-198)."""
+        for st, x in zip(self.states, X):
+            st.flag.zero_()
+            st.k.any_nonzero(x, st.flag)
+        self.comm.allreduce_max([st.flag for st in self.states])
+        return bool(int(self.states[0].flag.item()))
+
+    def iteration(self, F, W, R, Pv, Q, Z, recompute):
+        """One PCG iteration (solver.py:212-256) with every scalar on the
+        device: q = S p; p.q; alpha; r -= alpha q (w += alpha p deferred into
+        the p pass, or applied first when the residual is recomputed);
+        z = K_X r with r.z fused; beta; w/p update; the scalars copied to the
+        pinned host mirror.  No host synchronisation inside, so it can be
+        captured as one CUDA graph."""
+        self.schur(Pv, Q)
+        self.dot_dev(Pv, Q, 1)
+        for st, w, r, p, q in zip(self.states, W, R, Pv, Q):
+            st.k.pcg_scalar(0, st.scal)
+            st.k.pcg_update_wr(w, r, p, q, st.scal, recompute, not recompute)
+        if recompute:
+            self.schur(W, Z)
+            for st, f, z, r in zip(self.states, F, Z, R):
+                st.k.sub(f, z, r)
+        self.kx_dot_dev(R, Z, 2)
+        for st, w, p, z in zip(self.states, W, Pv, Z):
+            st.k.pcg_scalar(1, st.scal)
+            st.k.pcg_update_wp(w, p, z, st.scal, not recompute)
+            st.hscal.copy_(st.scal, non_blocking=True)
+
+    @property
+    def capturable(self):
+        return all(st.scal.is_cuda for st in self.states) and self.comm.capturable
 
     def axpy(self, a, X, Y):
         for st, x, y in zip(self.states, X, Y):
@@ -390,9 +471,15 @@ class SlabPCGResult:
 
 
 def pcg(system: SlabSystem, F, W, epsilon=0.0, rtol=0.0, max_iterations=200,
-        recompute_every=50):
+        recompute_every=50, graphs=None):
     """F, W: lists (one per local state) of wavelet-local arrays; W is
-    overwritten with the solution.  Same stopping rule as `api.pcg`."""
+    overwritten with the solution.  Same stopping rule as `api.pcg`.
+
+    Scalars stay on the device (hwg_pcg's kernels): each iteration ends with
+    ONE host synchronisation to read p.q, r.z, alpha and beta.  On CUDA with a
+    capturable communicator (one rank, or the in-process SimComm) every
+    iteration without residual recomputation is replayed as one CUDA graph
+    (``graphs=False`` forces plain launches)."""
     import torch
     if not (epsilon > 0) and not (rtol > 0):
         raise ValueError("tolerance must be positive")
@@ -403,39 +490,37 @@ def pcg(system: SlabSystem, F, W, epsilon=0.0, rtol=0.0, max_iterations=200,
     Q = [torch.empty_like(f) for f in F]
     for w in W:
         w.zero_()
-    if system.dot(F, F) == 0.0:
+    if not system.any_nonzero(F):
         return SlabPCGResult(0, [0.0])
-    rho = system.kx_dot(R, Z)
+    system.kx_dot_dev(R, Z, 0)                    # rho -> scal[0]
+    rho = system.read_scalar(0)
     hist = [math.sqrt(max(rho, 0.0))]
     eps = rtol * hist[0] if rtol > 0 else epsilon
     if rho <= eps ** 2:
         return SlabPCGResult(0, hist, seconds=time.perf_counter() - t0)
     for p_, z in zip(Pv, Z):
         p_.copy_(z)
+    use_graph = system.capturable if graphs is None else (graphs and system.capturable)
+    graph = None
     alphas, betas = [], []
     for it in range(1, max_iterations + 1):
-        system.schur(Pv, Q)
-        pq = system.dot(Pv, Q)
+        recompute = it % recompute_every == 0
+        if use_graph and not recompute:
+            if graph is None:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    system.iteration(F, W, R, Pv, Q, Z, False)
+            graph.replay()
+        else:
+            system.iteration(F, W, R, Pv, Q, Z, recompute)
+        _, pq, rho_new, alpha, beta = system.read_scalars()[:5]
         if not pq > 0:
             raise RuntimeError(f"operator lost positive definiteness (p^T S p = {pq:g})")
-        alpha = rho / pq
-        system.axpy(alpha, Pv, W)
-        if it % recompute_every == 0:
-            system.schur(W, Z)
-            for r, f, z in zip(R, F, Z):
-                r.copy_(f)
-            system.axpy(-1.0, Z, R)
-        else:
-            system.axpy(-alpha, Q, R)
-        rho_new = system.kx_dot(R, Z)
-        beta = rho_new / rho
         alphas.append(alpha)
         betas.append(beta)
-        rho = rho_new
-        hist.append(math.sqrt(max(rho, 0.0)))
-        if rho <= eps ** 2:
+        hist.append(math.sqrt(max(rho_new, 0.0)))
+        if rho_new <= eps ** 2:
             return SlabPCGResult(it, hist, alphas, betas, time.perf_counter() - t0)
-        system.xpay(beta, Z, Pv)
     from ._lib import IterationLimitError
     raise IterationLimitError(f"PCG did not reach tolerance {eps:g} within {max_iterations} "
                               "iterations", hist)
@@ -467,6 +552,11 @@ class CudaKernels:
         self.tree_sum = ctx.tree_sum
         self.axpy = ctx.axpy
         self.xpay = ctx.xpay
+        self.pcg_scalar = ctx.pcg_scalar
+        self.pcg_update_wr = ctx.pcg_update_wr
+        self.pcg_update_wp = ctx.pcg_update_wp
+        self.sub = ctx.sub
+        self.any_nonzero = ctx.any_nonzero
         self.spatial = ctx.spatial
         self.temporal_rows = ctx.temporal_rows
 

@@ -20,13 +20,15 @@ class NumpyKernels:
         self.stage = {j + 1: st for j, st in enumerate(system.wavelet.stages)}
 
     # --- wavelet stages with offsets -------------------------------------
-    def syn_stage(self, j, C, c0, Dw, d0, Y, f0, nf):
+    def syn_stage(self, j, C, c0, Dw, d0, Y, f0, nf, Dh=None):
         C, Dw, Y = _np(C), _np(Dw), _np(Y)
         nc, nfl = 2 ** (j - 1) + 1, 2 ** j + 1
         Xg = np.zeros((nfl, self.nx))
         for r in range(C.shape[0]):
             if 0 <= c0 + r < nc:
                 Xg[c0 + r] = C[r]
+        if Dh is not None and 0 <= d0 - 1 < nfl - nc:
+            Xg[nc + d0 - 1] = _np(Dh)
         for r in range(Dw.shape[0]):
             if 0 <= d0 + r < nfl - nc:
                 Xg[nc + d0 + r] = Dw[r]
@@ -111,6 +113,34 @@ class NumpyKernels:
 
     def xpay(self, a, X, Y):
         O.xpay(a, np.ascontiguousarray(_np(X)), _np(Y))
+
+    # --- device-scalar PCG steps (hwg_pcg_scalar / _update_wr / _update_wp)
+    def pcg_scalar(self, step, scal):
+        s = _np(scal)
+        if step == 0:
+            s[3] = s[0] / s[1]
+        else:
+            s[4] = s[2] / s[0]
+            s[0] = s[2]
+
+    def pcg_update_wr(self, w, r, p, q, scal, do_w, do_r):
+        a = float(_np(scal)[3])
+        if do_w:
+            self.axpy(a, p, w)
+        if do_r:
+            self.axpy(-a, q, r)
+
+    def pcg_update_wp(self, w, p, z, scal, do_w):
+        s = _np(scal)
+        if do_w:
+            self.axpy(float(s[3]), p, w)
+        self.xpay(float(s[4]), z, p)
+
+    def sub(self, f, t, r):
+        _np(r)[:] = _np(f) - _np(t)
+
+    def any_nonzero(self, X, flag):
+        _np(flag)[0] |= int(np.any(_np(X)))
 
     # --- temporal factor on a row range (distributed RHS) --------------------
     def temporal_rows(self, band, X, x0, Y, r0, nr):

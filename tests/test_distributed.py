@@ -236,3 +236,63 @@ def test_gpu_virtual_ranks_lshape(J, K, Ps):
         w = torch.empty_like(w1)
         ctx.grid_gather(wg, w)
         assert torch.equal(w, w1), (P, float((w - w1).abs().max()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,J,K", [(2, 6, 7), (2, 4, 10)])
+def test_nccl_world1_slab_matches_hwg_pcg(d, J, K):
+    """The time-slab solver under a real NCCL process group of one rank (the
+    bench's --slab / torchrun path at N = 1): device-resident scalars, the
+    iteration replayed as a CUDA graph, bit-identical to the single-GPU
+    hwg_pcg (same kernels, same reduction tree)."""
+    import torch.distributed as dist
+    import paper_2009_08875_b200 as hw
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** d
+    F = inputs.forcing("uniform", n_t, n_x)
+    asm = hw.assemble_system(hw.ProblemData(D=np.eye(d), c=0.0, u0=inputs.u0_sines), J, K,
+                             hw.SolveConfig(), forcing=F, host_rhs=False)
+    f = asm.rhs.f_hat.array
+    w1 = torch.empty_like(f)
+    stats, rc = asm.ctx.pcg(f, w1, 0.0, 1e-6)
+    assert rc == 0
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0,
+                            world_size=1, device_id=dev)
+    try:
+        states = D.make_states(d, J, K, 1, [0], lambda p: dev)
+        system = D.SlabSystem(states, D.TorchComm())
+        assert system.capturable
+        Fl = [D.scatter_wavelet(f, states[0].lay).clone()]
+        Wl = [torch.zeros_like(Fl[0])]
+        res = D.pcg(system, Fl, Wl, rtol=1e-6)
+        assert res.iterations == stats["iterations"]
+        assert res.residual_norms == stats["residual_norms"]
+        w = D.gather_wavelet(Wl, [states[0].lay], torch.zeros_like(f))
+        assert torch.equal(w, w1)
+        # plain launches give the same iterates as the graph replays
+        Wl2 = [torch.zeros_like(Fl[0])]
+        res2 = D.pcg(system, Fl, Wl2, rtol=1e-6, graphs=False)
+        assert res2.residual_norms == res.residual_norms and torch.equal(Wl2[0], Wl[0])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_zero_rhs_uses_any_nonzero():
+    """A right-hand side whose squared norm underflows to zero is still
+    non-zero (np.any(f), solver.py:196-198): the slab solver iterates."""
+    from slab_numpy import NumpyKernels
+    from oracle import heatwave_oracle as O
+    system = O.assemble(2, 3, 3)
+    n_t, n_x = system.shape
+    f = np.zeros((n_t, n_x))
+    f[3, 4] = 1e-170                         # f.f = 1e-340 -> 0.0 in fp64
+    assert O.dot(f, f) == 0.0 and np.any(f)
+    states = [D.RankState(D.slab_layout(3, 2, p), NumpyKernels(system), n_x, "cpu")
+              for p in range(2)]
+    sysd = D.SlabSystem(states, D.SimComm(2))
+    F = [D.scatter_wavelet(torch.from_numpy(f), st.lay).clone() for st in states]
+    assert sysd.any_nonzero(F)
+    Z = [torch.zeros_like(x) for x in F]
+    assert not sysd.any_nonzero(Z)
+    res = D.pcg(sysd, Z, [torch.zeros_like(x) for x in F], epsilon=1e-6)
+    assert res.iterations == 0 and res.residual_norms == [0.0]

@@ -419,3 +419,31 @@ def test_solve_host_pipelined_copy_matches_device_solve():
     assert st2["iterations"] == st["iterations"]
     assert st2["residual_norms"] == st["residual_norms"]
     assert np.array_equal(uh.numpy(), u_dev)
+
+
+def test_pcg_graph_follows_schur_form():
+    """The captured PCG iteration bakes in the Schur form: a test-space solve
+    after a five-term solve on the same context and the same w buffer must
+    apply the test-space operator -- bit-identical to a fresh test-space
+    context (and different from the five-term iterate)."""
+    J, K = 3, 6
+    n_t, n_x = 2 ** J + 1, (2 ** K - 1) ** 2
+    F = inputs.forcing("uniform", n_t, n_x)
+    prob = hw.ProblemData(D=np.eye(2), c=0.0, u0=inputs.u0_sines)
+    asm = hw.assemble_system(prob, J, K, hw.SolveConfig(), forcing=F, host_rhs=False)
+    ctx, f = asm.ctx, asm.rhs.f_hat.array
+    w = torch.empty_like(f)
+    s5, rc = ctx.pcg(f, w, 0.0, 1e-6)
+    assert rc == 0
+    w5 = w.clone()
+    ctx.set_schur_form("test_space")
+    sa, rc = ctx.pcg(f, w, 0.0, 1e-6)
+    assert rc == 0
+    fresh = hw.assemble_system(prob, J, K, hw.SolveConfig(form="test_space"), forcing=F,
+                               host_rhs=False)
+    w2 = torch.empty_like(f)
+    sb, rc = fresh.ctx.pcg(f, w2, 0.0, 1e-6)
+    assert rc == 0
+    assert sa["residual_norms"] == sb["residual_norms"]
+    assert torch.equal(w, w2)
+    assert not torch.equal(w, w5)

@@ -215,3 +215,26 @@ def test_bench_config5_workload_and_dof_bytes():
     assert abs(frac - 3141633 / 2047 ** 2) < 1e-15 and 0.74 < frac < 0.76
     assert bench.dof_fraction(4, 2, 10, 1023 ** 2) == 1.0
     assert "per-GPU share" in bench.workload_label(5, d, J, K, n_t, n_x)
+
+
+def test_bench_launcher_command():
+    """bench.py --gpus N (no WORLD_SIZE) re-runs itself as N torchrun ranks
+    on 127.0.0.1 with the same arguments."""
+    import bench
+    cmd = bench.launcher_command(["--gpus", "8", "--steps", "2"], 8, 29501)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd
+    i = cmd.index("--master-addr")
+    assert cmd[i + 1] == "127.0.0.1" and "--master-port=29501" in cmd
+    assert cmd[-5:] == [os.path.abspath(bench.__file__), "--gpus", "8", "--steps", "2"]
+
+
+def test_bench_configs_match_between_arms():
+    """Both arms print the same `config` object (the reference arm's bounded
+    sample is described in its cpu_baseline.sample)."""
+    import bench
+    for cfg in (1, 2, 3, 4):
+        assert bench.config_dict(cfg, 1)["dofs"] == (2 ** bench.workload(cfg)[1] + 1) * \
+            bench.workload(cfg)[6]
+    assert bench.config_dict(4, 8)["parallelism"].startswith("time slabs x8")
+    assert bench.config_dict(4, 1)["parallelism"] == "1 GPU"
