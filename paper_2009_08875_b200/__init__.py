@@ -15,6 +15,12 @@ from .api import (SolveConfig, SpaceTimeVector, TemporalDiscretization, MeshHier
                   assemble_system, assemble_rhs, PCGResult, pcg, solve_heat, HeatSolution,
                   measure_error, estimate_condition, lanczos_tridiagonal, lanczos_condition, ParallelPlan,
                   split_ranges, tree_reduce, project_initial, decaying_heat, forced_heat,
-                  PROBLEMS)
+                  PROBLEMS, build_prolongation, schur_apply, apply_KY, apply_KX, wavelet_apply,
+                  wavelet_transpose_apply, WorkerPool, parallel_execute)
+from .structures import (SparseMatrix, TemporalMatrices, TestMatrices, SpatialMatrices,
+                         WaveletLevels, csr_matvec, dense_materialize, assemble_temporal_trial,
+                         assemble_temporal_test, evaluate_trace, assemble_spatial,
+                         assemble_level_operators, build_wavelet)
+from .api import assemble_load
 
 __version__ = "0.1.0"

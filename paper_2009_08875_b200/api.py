@@ -19,6 +19,10 @@ from typing import Optional
 import numpy as np
 
 from . import discretization as disc
+from . import structures as _st
+from .structures import (SparseMatrix, TemporalMatrices, TestMatrices, SpatialMatrices,
+                         WaveletLevels, assemble_temporal_trial, assemble_temporal_test,
+                         assemble_spatial, assemble_level_operators, build_wavelet)
 from ._lib import IterationLimitError, check as _check
 from .device import GpuContext, as_device, _torch
 from .discretization import ProblemData, FineMesh
@@ -31,7 +35,9 @@ __all__ = [
     "HeatSolution", "measure_error", "estimate_condition", "lanczos_tridiagonal",
     "lanczos_condition",
     "ParallelPlan", "split_ranges", "tree_reduce", "ProblemData", "project_initial",
-    "decaying_heat", "forced_heat", "PROBLEMS",
+    "decaying_heat", "forced_heat", "PROBLEMS", "build_prolongation", "schur_apply",
+    "apply_KY", "apply_KX", "wavelet_apply", "wavelet_transpose_apply", "WorkerPool",
+    "parallel_execute", "assemble_load",
 ]
 
 
@@ -133,13 +139,38 @@ class MeshHierarchy:
         if domain not in ("square", "L") or (domain == "L" and (d != 2 or K < 2)):
             raise ValueError("domain must be 'square' or 'L' (2D, K >= 2)")
         self.d, self.K, self.domain = d, K, domain
-        self._finest = None
+        self._levels = {}
+        self._prols = {}
+        self.k0 = 2 if domain == "L" else 1        # the L's first level with interior dofs
+
+    def mesh(self, k) -> FineMesh:
+        """Level-k mesh (h = 2^-k), built on first use."""
+        if not self.k0 <= k <= self.K:
+            raise ValueError(f"no mesh level {k}")
+        if k not in self._levels:
+            self._levels[k] = FineMesh(self.d, k, self.domain)
+        return self._levels[k]
 
     @property
     def finest(self) -> FineMesh:
-        if self._finest is None:
-            self._finest = FineMesh(self.d, self.K, self.domain)
-        return self._finest
+        return self.mesh(self.K)
+
+    @property
+    def levels(self):
+        """Meshes coarse to fine (spatial.py:73-95)."""
+        return [self.mesh(k) for k in range(self.k0, self.K + 1)]
+
+    def prolongation(self, k) -> SparseMatrix:
+        """Interpolation from level k-1 interior dofs to level k."""
+        if not self.k0 + 1 <= k <= self.K:
+            raise ValueError(f"no prolongation onto level {k}")
+        if k not in self._prols:
+            self._prols[k] = _st.prolongation_between(self.mesh(k - 1), self.mesh(k))
+        return self._prols[k]
+
+    @property
+    def prolongations(self):
+        return [self.prolongation(k) for k in range(self.k0 + 1, self.K + 1)]
 
     @property
     def N_x(self):
@@ -150,8 +181,17 @@ def build_mesh_hierarchy(d: int, K: int, domain: str = "square") -> MeshHierarch
     return MeshHierarchy(d, K, domain)
 
 
+def build_prolongation(hierarchy: MeshHierarchy, k: int) -> SparseMatrix:
+    return hierarchy.prolongation(k)
+
+
 def project_initial(mesh: FineMesh, u0):
     return disc.project_initial(mesh, u0)
+
+
+def assemble_load(mesh: FineMesh, J: int, g) -> "SpaceTimeVector":
+    """Moments <g, xi_i (x) phi_j> against the test basis (spatial.py:269-300)."""
+    return SpaceTimeVector(disc.assemble_load(mesh, J, g))
 
 
 # --------------------------------------------------------------------------
@@ -204,6 +244,27 @@ class WaveletTransform:
 
     def transpose_apply_array(self, X, pool=None, out=None, scratch=None):
         return self._apply(X, True, out)
+
+    @property
+    def levels(self) -> WaveletLevels:
+        """Level map and two-scale matrices (host, built on first use)."""
+        if getattr(self, "_levels", None) is None:
+            self._levels = build_wavelet(self.ctx.J)
+        return self._levels
+
+    def apply(self, v):
+        return SpaceTimeVector(self.apply_array(v.array))
+
+    def transpose_apply(self, v):
+        return SpaceTimeVector(self.transpose_apply_array(v.array))
+
+
+def wavelet_apply(wt: WaveletTransform, v: SpaceTimeVector) -> SpaceTimeVector:
+    return SpaceTimeVector(wt.apply_array(v.array))
+
+
+def wavelet_transpose_apply(wt: WaveletTransform, v: SpaceTimeVector) -> SpaceTimeVector:
+    return SpaceTimeVector(wt.transpose_apply_array(v.array))
 
 
 # --------------------------------------------------------------------------
@@ -294,15 +355,48 @@ def make_solver(hierarchy: MeshHierarchy, alpha: float, mu: float, n_vcycles: in
 # --------------------------------------------------------------------------
 # the preconditioned Schur system (system.py:67-324)
 # --------------------------------------------------------------------------
-class SchurOperator:
-    """S-hat = W^T S W (five-term form) as a matrix-free GPU operator."""
+def _ctx_of(*objs):
+    """The one GPU context behind a set of operator components."""
+    ctxs = {id(o.ctx): o.ctx for o in objs if o is not None and getattr(o, "ctx", None) is not None}
+    if len(ctxs) != 1:
+        raise ValueError("operator components must come from one assembled GPU system "
+                         "(assemble_system)")
+    return next(iter(ctxs.values()))
 
-    def __init__(self, ctx: GpuContext, form="five_term"):
-        if form not in ("test_space", "five_term"):
+
+@dataclass
+class SchurOperator:
+    """S-hat = W^T S W as a matrix-free GPU operator (system.py:67-193).
+
+    Same fields as the reference dataclass, so ``dataclasses.replace(S,
+    form="test_space")`` works; the components must come from one
+    ``assemble_system`` (their GPU context carries the stencils, temporal
+    bands and multigrid hierarchy the kernels apply)."""
+
+    temporal: object = None
+    spatial: object = None
+    K_x: object = None
+    wavelet: object = None
+    form: str = "five_term"
+    test: object = None
+    ctx: GpuContext = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.form not in ("test_space", "five_term"):
             raise ValueError("form must be 'five_term' or 'test_space'")
-        self.ctx = ctx
-        self.form = form
-        ctx.set_schur_form(form)          # also the form pcg applies (SolveConfig.form)
+        if self.form == "test_space" and self.test is None:
+            raise ValueError("the test-space form needs the test matrices")
+        if self.ctx is None:
+            self.ctx = _ctx_of(self.K_x, self.wavelet)
+        own = getattr(self.ctx, "host_temporal", None)
+        if self.temporal is not None and own is not None and self.temporal is not own:
+            for name in ("M_t", "A_t", "L"):
+                a, b = getattr(self.temporal, name), getattr(own, name)
+                if (a.rows != b.rows or not np.array_equal(a.row_offsets, b.row_offsets)
+                        or not np.array_equal(a.col_indices, b.col_indices)
+                        or not np.array_equal(a.values, b.values)):
+                    raise NotImplementedError(
+                        f"the GPU operator's temporal factor {name} is fixed at assembly")
 
     @property
     def n_t(self):
@@ -326,14 +420,32 @@ class SchurOperator:
         return SpaceTimeVector(self.apply_array(v.array, pool))
 
 
-class PreconditionerKX:
-    """K_X = blockdiag[C_|lambda| A_x C_|lambda|] over wavelet coordinates."""
+def schur_apply(S: SchurOperator, w: SpaceTimeVector, pool=None) -> SpaceTimeVector:
+    return S.apply(w, pool)
 
-    def __init__(self, ctx: GpuContext, blocks: dict):
-        self.ctx = ctx
-        self.blocks = blocks
-        self.level_of = disc.level_of(ctx.J)
-        self.alpha = ctx.alpha
+
+@dataclass
+class PreconditionerKX:
+    """K_X = blockdiag[C_|lambda| A_x C_|lambda|] over wavelet coordinates
+    (system.py:211-279); blocks[j] is the C_j MultigridSolver of the same
+    assembled system (operator 1 + j of its context)."""
+
+    blocks: dict
+    A_x: object = None
+    level_of: np.ndarray = None
+    alpha: float = None
+    ctx: GpuContext = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.ctx is None:
+            self.ctx = _ctx_of(*self.blocks.values())
+        for j, b in self.blocks.items():
+            if getattr(b, "ctx", None) is not self.ctx or getattr(b, "op", None) != 1 + int(j):
+                raise ValueError(f"block {j} is not the C_{j} solver of this system")
+        if self.level_of is None:
+            self.level_of = disc.level_of(self.ctx.J)
+        if self.alpha is None:
+            self.alpha = self.ctx.alpha
 
     def apply_array(self, X, pool=None, out=None):
         for lvl in np.unique(self.level_of[: X.shape[0]]):
@@ -347,6 +459,24 @@ class PreconditionerKX:
 
     def apply(self, v: SpaceTimeVector, pool=None) -> SpaceTimeVector:
         return SpaceTimeVector(self.apply_array(v.array, pool))
+
+
+def apply_KX(P: PreconditionerKX, r: SpaceTimeVector, pool=None) -> SpaceTimeVector:
+    return P.apply(r, pool)
+
+
+def apply_KY(spatial, test, K_x, v: SpaceTimeVector) -> SpaceTimeVector:
+    """K_Y = O^-1 (x) K_x on a test-space vector (system.py:200-208): the
+    batched K_x V-cycles on every row (O = I, so the division is exact)."""
+    if v.n_t != test.O.rows:
+        raise ValueError(f"expected {test.O.rows} test-space rows, got {v.n_t}")
+    torch = _torch()
+    x, host = _in(K_x.ctx, v.array)
+    y = torch.empty_like(x)
+    K_x.ctx.mg_rows(K_x.op, x, y)
+    d = torch.as_tensor(test.O.diagonal(), device=y.device)[:, None]
+    y = y / d
+    return SpaceTimeVector(y.cpu().numpy() if host else y)
 
 
 class RightHandSide:
@@ -439,11 +569,17 @@ def assemble_system(problem: ProblemData, J: int, K: int, config: SolveConfig = 
     K_x = MultigridSolver(ctx, 0, 1.0, 0.0, config.vcycles, config.smooth, hier)
     blocks = {j: MultigridSolver(ctx, 1 + j, config.alpha, 2.0 ** j, config.vcycles,
                                  config.smooth, hier) for j in range(J + 1)}
-    S = SchurOperator(ctx, config.form)
-    KX = PreconditionerKX(ctx, blocks)
+    temporal = assemble_temporal_trial(J)
+    ctx.host_temporal = temporal
+    test = assemble_temporal_test(J)
+    spatial = _st.LazySpatialMatrices(hier.finest, problem.D, problem.c)
+    S = SchurOperator(temporal=temporal, spatial=spatial, K_x=K_x, wavelet=wt, form=config.form,
+                      test=test)
+    KX = PreconditionerKX(blocks=blocks, A_x=_st.LazyMatrix(spatial, "A_x"),
+                          level_of=disc.level_of(J), alpha=config.alpha)
     rhs = assemble_rhs(ctx, problem, hier.finest, forcing, host_rhs)
-    return ProblemAssembly(TemporalDiscretization(J), disc.temporal_values(J), None, hier,
-                           (ctx.stencil_M, ctx.stencil_A), wt, K_x, S, KX, rhs, ctx)
+    return ProblemAssembly(TemporalDiscretization(J), temporal, test, hier, spatial, wt, K_x, S,
+                           KX, rhs, ctx)
 
 
 # --------------------------------------------------------------------------
@@ -469,6 +605,38 @@ class ParallelPlan:
                 raise ValueError("ranges must be disjoint and contiguous")
             prev = b
         return self
+
+
+class WorkerPool:
+    """The reference's fork-join pool over temporal-column ranges
+    (solver.py:83-108).  On the GPU every row range of a phase runs in one
+    launch, so ``run_ranges`` calls ``fn(0, ncols)`` once; the reference's
+    results are identical for every worker count (test_solver.py:129-142),
+    so this changes no value."""
+
+    def __init__(self, n_workers: int = 1):
+        if n_workers < 1:
+            raise ValueError("need at least one worker")
+        self.n_workers = n_workers
+
+    def run_ranges(self, fn, ncols):
+        fn(0, ncols)
+
+    def close(self):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def parallel_execute(plan: "ParallelPlan", operator, v: SpaceTimeVector) -> SpaceTimeVector:
+    """One operator application under a worker plan (solver.py:303-309)."""
+    plan.validate()
+    with WorkerPool(plan.n_workers) as pool:
+        return operator.apply(v, pool)
 
 
 def split_ranges(n, parts):
@@ -532,11 +700,18 @@ def pcg(S: SchurOperator, K: PreconditionerKX, f_hat, epsilon: float,
         recompute_every: int = 50, rtol: float = 0.0) -> PCGResult:
     """PCG on S-hat w = f-hat, stopping on r^T K_X r <= eps^2 (device-resident).
 
+    ``plan`` (and SolveConfig.workers) is validated and otherwise has no
+    effect: the reference's iterates are bit-identical for every worker
+    count, and one GPU processes all temporal rows per launch (multi-GPU
+    time slabs: paper_2009_08875_b200.distributed).
+
     Extension: ``rtol > 0`` stops on sqrt(r^T K_X r) <= rtol sqrt(f^T K_X f)
     (the BASELINE rule); ``epsilon`` is then ignored."""
     torch = _torch()
     if not (epsilon > 0) and not (rtol > 0):
         raise ValueError("tolerance must be positive")
+    if plan is not None:
+        plan.validate()
     if S.ctx is not K.ctx:
         raise ValueError("S and K_X must come from the same assembled system")
     ctx = S.ctx

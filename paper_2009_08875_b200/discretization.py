@@ -262,6 +262,16 @@ class FineMesh:
         else:
             self.elements = elems
             self.interior = np.nonzero(np.all((gi > 0) & (gi < n), axis=1))[0]
+        self.interior_index = np.full(len(self.vertices), -1, dtype=np.int64)
+        self.interior_index[self.interior] = np.arange(len(self.interior))
+
+    @property
+    def level(self):          # the reference's Mesh.level (spatial.py:49-64)
+        return self.K
+
+    @property
+    def h(self):
+        return 2.0 ** -self.K
 
     @property
     def n_interior(self):

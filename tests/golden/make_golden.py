@@ -166,7 +166,7 @@ def run_case(name, d, J, K, dist, full=True, workers=8, lean=False, D=None, c=0.
                 u_norm=float(np.linalg.norm(u)),
                 w_norm=float(np.linalg.norm(res.w.array)),
                 stencils=stencil_table(asm, problem))
-    arrays = dict(u0proj=u0proj)
+    arrays = dict(u0proj=u0proj) if nsample <= 4096 else {}   # large twins: K = 10 rows are 8 MB
     rng = np.random.default_rng(PROBE_SEED)
     idx = np.sort(rng.choice(n_t * n_x, size=min(nsample, n_t * n_x), replace=False))
     arrays["sample_idx"] = idx
@@ -320,6 +320,50 @@ def check_interpolant_load():
         assert rel < 1e-13
 
 
+def struct_case(name="struct"):
+    """The reference's host-side containers on small problems: temporal
+    trial/test matrices, meshes, prolongations, level operators (also with
+    anisotropic D and reaction), wavelet two-scale matrices -- every CSR as
+    (row_offsets, col_indices, values)."""
+    from heatwave.multigrid import assemble_level_operators
+    arrays, meta = {}, dict(name=name, cases=[])
+
+    def put(key, m):
+        arrays[key + ".ip"], arrays[key + ".ix"] = m.row_offsets, m.col_indices
+        arrays[key + ".v"] = m.values
+        arrays[key + ".shape"] = np.array([m.rows, m.cols])
+
+    for J in (0, 1, 3):
+        tr, te = hw.assemble_temporal_trial(J), hw.assemble_temporal_test(J)
+        for f in ("M_t", "A_t", "L", "Gamma0"):
+            put(f"J{J}.{f}", getattr(tr, f))
+        arrays[f"J{J}.phi0"], arrays[f"J{J}.phiT"] = tr.phi_at_0, tr.phi_at_T
+        for f in ("O", "T", "N"):
+            put(f"J{J}.{f}", getattr(te, f))
+        lv = hw.build_wavelet(J)
+        arrays[f"J{J}.level_of"] = lv.level_of
+        for j, (P, Q) in enumerate(lv.two_scale, start=1):
+            put(f"J{J}.P{j}", P), put(f"J{J}.Q{j}", Q)
+            put(f"J{J}.M{j}", lv.stage_mats[j - 1][0]), put(f"J{J}.MT{j}", lv.stage_mats[j - 1][1])
+    for d, K, D, c in ((1, 4, None, 0.0), (2, 3, None, 0.0), (2, 4, [[1.0, 0.0], [0.0, 6.0]], 0.5)):
+        tag = f"d{d}K{K}" + ("a" if D is not None else "")
+        meta["cases"].append(dict(tag=tag, d=d, K=K, D=D, c=c))
+        hier = hw.build_mesh_hierarchy(d, K)
+        for k, m in enumerate(hier.levels, start=1):
+            arrays[f"{tag}.mesh{k}.vertices"] = m.vertices
+            arrays[f"{tag}.mesh{k}.elements"] = m.elements
+            arrays[f"{tag}.mesh{k}.interior"] = m.interior
+            arrays[f"{tag}.mesh{k}.interior_index"] = m.interior_index
+        for k in range(2, K + 1):
+            put(f"{tag}.P{k}", hier.prolongation(k))
+        for k, ops in enumerate(assemble_level_operators(hier, D, c), start=1):
+            put(f"{tag}.M{k}", ops.M_x), put(f"{tag}.A{k}", ops.A_x)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+    with open(os.path.join(HERE, f"{name}.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print(f"{name}: {len(arrays)} arrays", flush=True)
+
+
 CASES = {
     "c1": lambda: run_case("c1", 2, 4, 4, "uniform"),
     "d1": lambda: run_case("d1", 1, 6, 6, "normal"),
@@ -353,6 +397,7 @@ CASES = {
     # 1D J = 16, K = 10 (cfg 3's N_x, 65,537 temporal rows)
     "d16": lambda: run_case("d16", 1, 16, 10, "normal", full=False, nsample=65536),
     "load": check_interpolant_load,
+    "struct": struct_case,
 }
 
 if __name__ == "__main__":

@@ -4,6 +4,8 @@ GPU package (tests/test_solver.py, test_multigrid.py, test_acceptance.py of
 exact-inverse mode (ExactSolver, sparse LU) or 3D meshes are not restated:
 both are outside the GPU hot path.  The oracle (tests only)
 supplies the P1 mass matrix where a reference test assembles one."""
+import dataclasses
+
 import numpy as np
 import pytest
 import scipy.sparse.linalg as spla
@@ -198,7 +200,7 @@ def test_symmetry(hier2d, rng):                                # test_multigrid.
 # ---- test_acceptance.py: criterion 2 (Schur forms agree) --------------------
 def test_forms_agree_on_random_vectors(rng):                    # test_acceptance.py:85-98
     asm = hw.assemble_system(hw.decaying_heat(2), 3, 3, hw.SolveConfig())
-    S1 = hw.SchurOperator(asm.ctx, "test_space")
+    S1 = dataclasses.replace(asm.S, form="test_space")
     worst = 0.0
     for _ in range(100):
         v = hw.SpaceTimeVector(rng.standard_normal((9, 49)))
