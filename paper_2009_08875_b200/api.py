@@ -575,6 +575,7 @@ def assemble_system(problem: ProblemData, J: int, K: int, config: SolveConfig = 
     spatial = _st.LazySpatialMatrices(hier.finest, problem.D, problem.c)
     S = SchurOperator(temporal=temporal, spatial=spatial, K_x=K_x, wavelet=wt, form=config.form,
                       test=test)
+    ctx.set_schur_form(config.form)          # the form hwg_pcg applies (SolveConfig.form)
     KX = PreconditionerKX(blocks=blocks, A_x=_st.LazyMatrix(spatial, "A_x"),
                           level_of=disc.level_of(J), alpha=config.alpha)
     rhs = assemble_rhs(ctx, problem, hier.finest, forcing, host_rhs)

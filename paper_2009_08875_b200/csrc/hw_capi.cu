@@ -57,7 +57,7 @@ struct hwg_ctx {
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
     int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
-    int mg1d_fused = 1;                 // 1D, K >= 6: fused-sweep kernel (HWG_MG1D=0: hw_mg1d.cu)
+    int mg1d_fused = 0;                 // 1D, K >= 6: 128-thread fused-sweep kernel (HWG_MG1D=1)
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
     int form = 0;                      // S: 0 five-term (Lemma 2), 1 test-space (Lemma 1)
@@ -600,7 +600,7 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     if (const char *ev = getenv("HWG_COARSE_EXACT"))        // A/B switch for measurements
         if (ev[0] == '1') c->coarse_fast = 0;
     if (const char *ev = getenv("HWG_MG1D"))                // A/B switch for measurements
-        if (ev[0] == '0') c->mg1d_fused = 0;
+        if (ev[0] == '1') c->mg1d_fused = 1;
     if (const char *ev = getenv("HWG_GRAPH"))               // A/B switch for measurements
         if (ev[0] == '0') c->use_graph = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask
