@@ -464,7 +464,7 @@ static int schur(hwg_ctx *c, const double *X, double *Y, cudaStream_t st)
     TRY(wavelet(c, X, c->U, c->T12, c->T12 + N, false, st));
     // t1 = A_t MxU + L^T AxU, t1' = M_t AxU + L MxU (one pass over U); the
     // first row of MxU is kept for the trace term
-    CK(launch_bside_fused(c->U, 0, c->T12, c->T12 + N, c->MxU, c->grid, c->SM, c->SA,
+    CK(launch_bside_fused(c->U, 0, nt, c->T12, c->T12 + N, c->MxU, c->grid, c->SM, c->SA,
                           Tri4{c->At.tri, c->LT.tri, c->Mt.tri, c->L.tri}, 0, nt, nt, st));
     ++c->launches;
     TRY(mg_apply(c, c->T12, c->G12, 2 * nt, 0, nullptr, st));
@@ -1229,7 +1229,7 @@ int hwg_bside_rows(hwg_ctx *c, const double *U, int64_t u0, int64_t nu, double *
     if (u0 > (r0 > 0 ? r0 - 1 : 0) || u0 + nu < (r0 + nr < c->nt ? r0 + nr + 1 : r0 + nr))
         return fail(HWG_EINVAL, "U does not cover the rows the temporal bands need");
     if (nr == 0) return HWG_OK;
-    CK(launch_bside_fused(U, u0, T1, T2, r0 == 0 ? E0 : nullptr, c->grid, c->SM, c->SA,
+    CK(launch_bside_fused(U, u0, nu, T1, T2, r0 == 0 ? E0 : nullptr, c->grid, c->SM, c->SA,
                           Tri4{c->At.tri, c->LT.tri, c->Mt.tri, c->L.tri}, r0, nr, c->nt,
                           S(stream)));
     ++c->launches;

@@ -112,9 +112,10 @@ cudaError_t launch_bt_side(const double *G1, const double *G2, const double *E0,
                            Grid g, Stencil M, Stencil A, int64_t rows, cudaStream_t st);
 cudaError_t launch_temporal_bands(BandOut o1, BandOut o2, int64_t rows, int64_t nx,
                                   cudaStream_t st);
-cudaError_t launch_bside_fused(const double *U, int64_t u0, double *T1, double *T2, double *E0,
-                               Grid g, Stencil M, Stencil A, Tri4 tri, int64_t r0, int64_t nr,
-                               int64_t nt, cudaStream_t st);
+// U holds nu temporal rows starting at global row u0 (the readable extent)
+cudaError_t launch_bside_fused(const double *U, int64_t u0, int64_t nu, double *T1, double *T2,
+                               double *E0, Grid g, Stencil M, Stencil A, Tri4 tri, int64_t r0,
+                               int64_t nr, int64_t nt, cudaStream_t st);
 cudaError_t launch_add(const double *X1, const double *X2, double *Y, int64_t total,
                        cudaStream_t st);
 // L-shaped domain: rows of the lexicographic dof layout (nxu per row) <-> the
