@@ -32,6 +32,11 @@
 //    zero-filling cp.async into THREAD-PRIVATE shared-memory slots three
 //    steps ahead, so they need no barrier; each step has two barriers
 //    (halo exchange, carry exchange).
+//  * Scaled iterates: inside a pass every row the sweeps touch holds c0 x
+//    (x0 rows are scaled once as they are loaded, final rows unscaled once
+//    as they are staged for the store), so a point's update needs no b / c0:
+//    c0 x = b - (cx/c0)(c0 u + c0 d) - ... + beta c0 x_left.  DOWN's GS-identity
+//    residual of scaled differences is then the residual itself.
 //  * LSH: the mapped L-shaped domain, embedded in the square grid with the
 //    closed quadrant i, j >= m = (n-1)/2 (natural coordinates) held at zero.
 //    Lexicographic GS on the L is GS on the square with those points reset
@@ -373,7 +378,7 @@ struct RegPass {
         if constexpr (DOWN) v[P] = slot[hoff];                         // right halo
         else if constexpr (LR == 0) v[P] = slot[ooff[P / 2] + 1];
         if constexpr (!DOWN) {
-            if (EDGE && i >= n) return;                  // row n stays a zero pad
+            if (EDGE && i >= n) return;                  // row n stays a zero pad (no scaling)
             // coarse rows c_a = floor((i-1)/2) and, for even i, c_a + 1.  Row
             // c_a is the one the previous step loaded (kept as exact halves in
             // HC), so each pair of steps reads one new coarse row.  0.5 c is
@@ -412,6 +417,8 @@ struct RegPass {
             }
             if (last) v[P - 1] = v[P] = 0.0;             // columns n, n+1
         }
+#pragma unroll
+        for (int e = 0; e <= P; ++e) v[e] *= c0;         // the pass works on c0 x
     }
 
     template <int LR>
@@ -477,9 +484,9 @@ struct RegPass {
             const double ul = k ? u[k - 1] : uL;
             const double cr = k < P - 1 ? c[k + 1] : cR;
             const double dr = k < P - 1 ? d[k + 1] : dR;
-            // p = (b - cd (ul + dr) - cx (u + d) - cy cr) / c0 with the
-            // coefficients pre-scaled by 1/c0 (7 FP64 operations per point)
-            double pv = fma(beta, cr, b[k] * inv);
+            // c0 y = b - (cd/c0)(ul + dr) - (cx/c0)(u + d) - (cy/c0) cr on
+            // rows scaled by c0 (6 FP64 operations per point)
+            double pv = fma(beta, cr, b[k]);          // rows hold c0 x: no b / c0
             if constexpr (DG) pv = fma(-cds, ul + dr, pv);
             pv = fma(-cxs, u[k] + d[k], pv);
             yy = fma(beta, yy, pv);
@@ -542,7 +549,7 @@ struct RegPass {
             for (int k = 0; k < P; ++k) {
                 const double d6r = k < P - 1 ? D[PAR][k + 1] : DR[PAR];
                 const double d5r = k < P - 1 ? D[Q][k + 1] : DR[Q];
-                // residual / c0 (the coarse right-hand side is scaled back by c0)
+                // the residual (differences of scaled rows: no c0 factor)
                 R[k] = DG ? fma(beta, d6r, fma(-cxs, D[Q][k], -cds * d5r))
                           : fma(beta, d6r, -cxs * D[Q][k]);
             }
@@ -591,7 +598,7 @@ struct RegPass {
         for (int h = 0; h < P / 2; ++h) {
             const int u = (P / 2) * tid + h;
             *reinterpret_cast<double2 *>(osm + ((u ^ ((u >> 3) & SWZ)) << 1)) =
-                make_double2(xn[2][2 * h], xn[2][2 * h + 1]);
+                make_double2(xn[2][2 * h] * inv, xn[2][2 * h + 1] * inv);   // unscale
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -632,7 +639,7 @@ struct RegPass {
                         acc[q] += fma(0.5, r0 + r2, r1);
                     } else {                             // bottom of r/2-1, top of r/2
                         if (r >= 2 && (q < P / 2 - 1 || !last))
-                            Bcg[(int64_t)(r / 2 - 1) * m + q] = c0 * (acc[q] + 0.5 * (r1 + r2));
+                            Bcg[(int64_t)(r / 2 - 1) * m + q] = acc[q] + 0.5 * (r1 + r2);
                         acc[q] = 0.5 * (r0 + r1);
                     }
                 }
