@@ -151,9 +151,15 @@ struct ProfScope {
     int cls;
     double bytes;
     cudaEvent_t a{}, b{};
+    bool on = false;
     ProfScope(hwg_ctx *c_, cudaStream_t s, int k, double by) : c(c_), st(s), cls(k), bytes(by)
     {
-        if (c->prof) {
+        // never inside a stream capture (a caller's CUDA graph): events
+        // recorded there cannot be timed
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        on = c->prof && cudaStreamIsCapturing(st, &cs) == cudaSuccess &&
+             cs == cudaStreamCaptureStatusNone;
+        if (on) {
             if (c->prof_recs.size() > 4096) prof_flush(c);
             a = prof_event(c);
             cudaEventRecord(a, st);
@@ -161,7 +167,7 @@ struct ProfScope {
     }
     ~ProfScope()
     {
-        if (c->prof) {
+        if (on) {
             b = prof_event(c);
             cudaEventRecord(b, st);
             c->prof_recs.push_back({a, b, cls, bytes});
@@ -410,7 +416,8 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                     a.dot_part = dot_part + r0;
                 }
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
-                ProfScope ps(c, st, l == c->K ? 1 : 3, 8.0 * nr * (3 * n2 + m2));
+                // b, x0, coarse x in, x out (+ the fused inner product's operand)
+                ProfScope ps(c, st, l == c->K ? 1 : 3, 8.0 * nr * (3 * n2 + m2 + (a.dot_y ? n2 : 0)));
                 CK(mg2d_stream_launch(a, false, nr, st));
                 ++c->launches;
             }

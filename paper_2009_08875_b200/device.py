@@ -110,8 +110,11 @@ class GpuContext:
     PROFILE_CLASSES = ("mg2d_down_finest", "mg2d_up_finest", "mg2d_down_coarser",
                        "mg2d_up_coarser", "mg2d_coarse", "mg1d")
 
+    profiling = False
+
     def profile_enable(self, on=True):
         _lib.check(self.lib.hwg_profile_enable(self.handle, int(on)))
+        self.profiling = bool(on)
 
     def profile_read(self):
         """{class: (ms, bytes, launches)} since profile_enable."""

@@ -447,7 +447,9 @@ class SlabSystem:
 
     @property
     def capturable(self):
-        return all(st.scal.is_cuda for st in self.states) and self.comm.capturable
+        # per-launch profiling events (hwg_profile_enable) need plain launches
+        profiling = any(getattr(getattr(st.k, "ctx", None), "profiling", False) for st in self.states)
+        return all(st.scal.is_cuda for st in self.states) and self.comm.capturable and not profiling
 
     def axpy(self, a, X, Y):
         for st, x, y in zip(self.states, X, Y):
