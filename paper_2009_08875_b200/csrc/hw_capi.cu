@@ -58,6 +58,8 @@ struct hwg_ctx {
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
     int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
     int mg1d_fused = 0;                 // 1D, K >= 6: 128-thread fused-sweep kernel (HWG_MG1D=1)
+    double *cmat1d = nullptr;           // 1D, K >= 6: [op][15][15] level-4 V-cycle operators
+    int mg1d_dense = 1;                 // HWG_MG1D_DENSE=0: the level-4..1 sub-cycle (A/B)
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
     int form = 0;                      // S: 0 five-term (Lemma 2), 1 test-space (Lemma 1)
@@ -346,7 +348,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
         double *Xp = X + r0 * c->nx;
         const int32_t *ro = row_op ? row_op + r0 : nullptr;
         if (c->dim == 1) {
-            Mg1dArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, ro, op, nr};
+            Mg1dArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, ro, op, nr, c->cmat1d};
             ProfScope ps(c, st, 5, 16.0 * nr * c->nx);
             CK(c->mg1d_fused && c->K >= 6 ? mg1d_fused_launch(a, st) : mg1d_launch(a, st));
             ++c->launches;
@@ -527,6 +529,33 @@ static int from_grid(hwg_ctx *c, const double *src, double *dst, int64_t rows, c
     return HWG_OK;
 }
 
+// 1D: the V-cycle from level kMg1dCut (zero start) of every operator as a
+// dense matrix, M[op][i][j] = (MG e_i)_j -- computed by the same multigrid
+// kernel on unit right-hand sides, so mg1d_reg's dense application is the
+// identical linear map (up to rounding)
+static int build_coarse_1d(hwg_ctx *c)
+{
+    if (!c->mg1d_dense) return HWG_OK;
+    const int nops = c->J + 2, n = kMg1dCutN;
+    const int64_t rows = (int64_t)nops * n;
+    std::vector<double> eye((size_t)rows * n, 0.0);
+    std::vector<int32_t> ops(rows);
+    for (int o = 0; o < nops; ++o)
+        for (int i = 0; i < n; ++i) {
+            eye[((size_t)o * n + i) * n + i] = 1.0;
+            ops[o * n + i] = o;
+        }
+    double *B = nullptr;
+    int32_t *dops = nullptr;
+    TRY(upload(c, &B, eye));
+    TRY(upload(c, &dops, ops));
+    TRY(dalloc(c, &c->cmat1d, rows * n));
+    Mg1dArgs a{B, n, c->cmat1d, n, c->coef, c->K + 1, kMg1dCut, 1, dops, 0, rows, nullptr};
+    CK(mg1d_launch(a, 0));
+    CK(cudaDeviceSynchronize());
+    return HWG_OK;
+}
+
 static int ensure_pcg(hwg_ctx *c)
 {
     if (c->r) return HWG_OK;
@@ -606,6 +635,8 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         else if (ev[0] == '5' && c->mg_reg_ok) c->mg_reg_ok = 3;   // P = 4 for UP at n = 1023
     if (const char *ev = getenv("HWG_COARSE_EXACT"))        // A/B switch for measurements
         if (ev[0] == '1') c->coarse_fast = 0;
+    if (const char *ev = getenv("HWG_MG1D_DENSE"))          // A/B switch for measurements
+        if (ev[0] == '0') c->mg1d_dense = 0;
     if (const char *ev = getenv("HWG_MG1D"))                // A/B switch for measurements
         if (ev[0] == '1') c->mg1d_fused = 1;
     if (const char *ev = getenv("HWG_GRAPH"))               // A/B switch for measurements
@@ -637,6 +668,7 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     for (int64_t r = 0; r < c->nt; ++r) ops[r] = 1 + c->level_of[r];
     GO(upload(c, &c->row_op_kx, ops));
     GO(build_temporal(c));
+    if (d.dim == 1 && d.K > kMg1dCut + 1) GO(build_coarse_1d(c));
     if (!c->kernel_only) {
         GO(dalloc(c, &c->U, c->N));
         GO(dalloc(c, &c->MxU, c->N));

@@ -63,7 +63,14 @@ struct Mg1dArgs {
     const int32_t *row_op;
     int op;
     int64_t rows;
+    // optional [op][15][15]: the V-cycle from level 4 (zero start) as a dense
+    // operator, M[op][i][j] = (MG_4 e_i)_j (hwg_create builds it by running
+    // this kernel with K = 4 on unit rows); mg1d_reg applies it instead of
+    // the level-4..1 sub-cycle
+    const double *cmat = nullptr;
 };
+constexpr int kMg1dCut = 4;                    // levels <= kMg1dCut: dense operator
+constexpr int kMg1dCutN = (1 << kMg1dCut) - 1;  // 15
 cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
 // K = 6..10: three sweeps per pass fused into one carry scan, 128-thread CTA
 // per temporal row (hw_mg1d_fused.cu); cudaErrorNotSupported otherwise

@@ -154,13 +154,37 @@ __device__ __forceinline__ void smooth_level(double *xw, double *bw, const doubl
 
 // pre-smoothing + restriction from level L down, the 1x1 coarse solve, then
 // prolongation + post-smoothing back up to L (all in shared memory)
-template <int L>
-__device__ __forceinline__ void down_from(double *xw, double *bw, const double *coef, int lane)
+// x_4 = M b_4: the level-4 V-cycle (zero start) as a dense 15 x 15 operator
+// staged in shared memory (cm: [i][j], lane j sums over i)
+__device__ __forceinline__ void coarse_dense(double *xw, const double *bw, const double *cm, int lane)
 {
+    constexpr int n = kMg1dCutN;
+    const double *b = bw + Lv<kMg1dCut>::off;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (lane < n) {
+#pragma unroll
+        for (int i = 0; i < n; i += 2) {
+            acc0 = fma(cm[i * n + lane], b[Lv<kMg1dCut>::at(i)], acc0);
+            if (i + 1 < n) acc1 = fma(cm[(i + 1) * n + lane], b[Lv<kMg1dCut>::at(i + 1)], acc1);
+        }
+    }
+    __syncwarp();
+    if (lane < n) xw[Lv<kMg1dCut>::off + Lv<kMg1dCut>::at(lane)] = acc0 + acc1;
+    __syncwarp();
+}
+
+template <int L>
+__device__ __forceinline__ void down_from(double *xw, double *bw, const double *coef, int lane,
+                                          const double *cm = nullptr)
+{
+    if (L == kMg1dCut && cm) {
+        coarse_dense(xw, bw, cm, lane);
+        return;
+    }
     if constexpr (L >= 2) {
         smooth_level<L>(xw, bw, coef, true, lane);
         residual_restrict<L>(xw, bw, coef + L * kCoefStride, lane);
-        down_from<L - 1>(xw, bw, coef, lane);
+        down_from<L - 1>(xw, bw, coef, lane, cm);
         prolongate_smem<L>(xw, lane);
         smooth_level<L>(xw, bw, coef, false, lane);
     } else {
@@ -211,8 +235,13 @@ __global__ void __launch_bounds__(32 * WPB, 1) mg1d_reg(Mg1dArgs a, int words)
     constexpr int ntot = Lv<K - 1>::off + Lv<K - 1>::size;   // levels 1..K-1
     double *xw = sm + (size_t)w * words;
     double *bw = xw + ntot;
+    double *cm = a.cmat ? bw + ntot : nullptr;                // this row's dense coarse operator
     const int op = a.row_op ? a.row_op[row] : a.op;
     const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
+    if (cm) {
+        const double *g = a.cmat + (int64_t)op * kMg1dCutN * kMg1dCutN;
+        for (int e = lane; e < kMg1dCutN * kMg1dCutN; e += 32) cm[e] = g[e];
+    }
     const double *cK = coef + K * kCoefStride;
     const double c0 = cK[kC0], oc = cK[kCy], inv = cK[kInv];
     const double beta = -oc * inv;
@@ -220,14 +249,22 @@ __global__ void __launch_bounds__(32 * WPB, 1) mg1d_reg(Mg1dArgs a, int words)
     const int nK = (1 << K) - 1;
     const int ncK = (1 << (K - 1)) - 1;
 
+    // the row's b: coalesced loads staged through the (not yet used) level
+    // storage with one pad per 32 points (a lane's chunk reads are then
+    // bank-conflict free), instead of CF strided loads per lane
+    static_assert(2 * ntot >= 32 * CF + CF, "staging fits in the coarse-level storage");
     double x[CF], b[CF];
     {
-        const double *Bg = a.B + row * a.ldB + lane * CF;
+        const double *Bg = a.B + row * a.ldB;
+        for (int j = lane; j < nK; j += 32) xw[j + j / CF] = Bg[j];
+        __syncwarp();
 #pragma unroll
         for (int k = 0; k < CF; ++k) {
-            b[k] = (lane * CF + k < nK) ? Bg[k] : 0.0;
+            const int j = lane * CF + k;
+            b[k] = (j < nK) ? xw[j + j / CF] : 0.0;
             x[k] = 0.0;
         }
+        __syncwarp();
     }
     double gam = beta;                                  // beta^CF
 #pragma unroll
@@ -336,7 +373,7 @@ __global__ void __launch_bounds__(32 * WPB, 1) mg1d_reg(Mg1dArgs a, int words)
             }
             __syncwarp();
         }
-        down_from<K - 1>(xw, bw, coef, lane);
+        down_from<K - 1>(xw, bw, coef, lane, cm);
         // prolongate into the registers: fine j = lane CF + k
         {
             const double *xc = xw + Lv<K - 1>::off;
@@ -358,17 +395,20 @@ __global__ void __launch_bounds__(32 * WPB, 1) mg1d_reg(Mg1dArgs a, int words)
         }
         for (int s = 0; s < 3; ++s) sweep(false);
     }
-    double *Xg = a.X + row * a.ldX + lane * CF;
+    // coalesced store through the same staging layout
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < CF; ++k)
-        if (lane * CF + k < nK) Xg[k] = x[k];
+    for (int k = 0; k < CF; ++k) xw[lane * CF + k + lane] = x[k];     // j + j / CF, j = lane CF + k
+    __syncwarp();
+    double *Xg = a.X + row * a.ldX;
+    for (int j = lane; j < nK; j += 32) Xg[j] = xw[j + j / CF];
 }
 
 template <int K, int WPB = 8>
 static cudaError_t launch_reg(const Mg1dArgs &a, cudaStream_t st)
 {
     const int ntot = Lv<K - 1>::off + Lv<K - 1>::size;
-    const int words = 2 * ntot + 1;
+    const int words = 2 * ntot + 1 + (a.cmat ? kMg1dCutN * kMg1dCutN : 0);
     const size_t smem = (size_t)WPB * words * sizeof(double);
     auto k = mg1d_reg<K, WPB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

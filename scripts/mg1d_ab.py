@@ -34,10 +34,11 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
 tag = os.environ.get("HWG_MG1D", "0")
+tag = tag + os.environ.get("HWG_MG1D_DENSE", "1")
 np.save(f"/tmp/mg1d_X_{tag}.npy", X[:64].cpu().numpy())
 print(f"HWG_MG1D={tag} J={J} rows={n_t}: {ms:.3f} ms per batch, {ms * 1e3 / n_t * 1e3:.1f} ns/row, "
       f"{16.0 * n_t * n_x / ms / 1e6:.1f} GB/s (b in, x out)")
-other = "/tmp/mg1d_X_0.npy" if tag == "1" else None
+other = "/tmp/mg1d_X_00.npy" if tag != "00" else None
 if other and os.path.exists(other):
     A = np.load(other)
     Bf = X[:64].cpu().numpy()
