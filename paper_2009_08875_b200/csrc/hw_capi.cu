@@ -57,7 +57,6 @@ struct hwg_ctx {
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
     int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
-    int mg1d_fused = 0;                 // 1D, K >= 6: 128-thread fused-sweep kernel (HWG_MG1D=1)
     double *cmat1d = nullptr;           // 1D, K >= 6: [op][15][15] level-4 V-cycle operators
     int mg1d_dense = 1;                 // HWG_MG1D_DENSE=0: the level-4..1 sub-cycle (A/B)
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
@@ -350,7 +349,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
         if (c->dim == 1) {
             Mg1dArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, ro, op, nr, c->cmat1d};
             ProfScope ps(c, st, 5, 16.0 * nr * c->nx);
-            CK(c->mg1d_fused && c->K >= 6 ? mg1d_fused_launch(a, st) : mg1d_launch(a, st));
+            CK(mg1d_launch(a, st));
             ++c->launches;
             continue;
         }
@@ -637,8 +636,6 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         if (ev[0] == '1') c->coarse_fast = 0;
     if (const char *ev = getenv("HWG_MG1D_DENSE"))          // A/B switch for measurements
         if (ev[0] == '0') c->mg1d_dense = 0;
-    if (const char *ev = getenv("HWG_MG1D"))                // A/B switch for measurements
-        if (ev[0] == '1') c->mg1d_fused = 1;
     if (const char *ev = getenv("HWG_GRAPH"))               // A/B switch for measurements
         if (ev[0] == '0') c->use_graph = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask

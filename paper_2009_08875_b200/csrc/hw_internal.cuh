@@ -72,9 +72,7 @@ struct Mg1dArgs {
 constexpr int kMg1dCut = 4;                    // levels <= kMg1dCut: dense operator
 constexpr int kMg1dCutN = (1 << kMg1dCut) - 1;  // 15
 cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
-// K = 6..10: three sweeps per pass fused into one carry scan, 128-thread CTA
-// per temporal row (hw_mg1d_fused.cu); cudaErrorNotSupported otherwise
-cudaError_t mg1d_fused_launch(const Mg1dArgs &a, cudaStream_t st);
+
 
 // ---- hw_wavelet.cu -------------------------------------------------------
 // mask_n > 0: columns are points of an mask_n x mask_n grid whose quadrant
