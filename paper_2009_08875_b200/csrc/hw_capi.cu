@@ -571,7 +571,7 @@ static int ensure_pcg(hwg_ctx *c)
 extern "C" {
 
 const char *hwg_last_error(void) { return g_err.c_str(); }
-int hwg_version(void) { return 4; }
+int hwg_version(void) { return 5; }
 
 int hwg_create(const hwg_desc *desc, hwg_ctx **out)
 {

@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert set(_lib.EXPORTS) == syms
     L = _lib.load()
-    assert L.hwg_version() == 4
+    assert L.hwg_version() == 5
 
 
 def test_library_is_sm100a():
