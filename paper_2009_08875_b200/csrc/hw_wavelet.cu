@@ -21,6 +21,7 @@
 #include "hw_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace hw {
 
@@ -126,6 +127,190 @@ __global__ void __launch_bounds__(kWavBS) wav_ana_pairs(const double *__restrict
             Dout[(int64_t)r * nx + i] = dd;
             xm = x1;
             x0 = x2;
+        }
+        Cout[(int64_t)r * nx + i] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two stages in one pass (the top stages carry nearly all of a transform's
+// bytes: stage J moves 2^J + 1 rows, J-1 half that).  Synthesis stages j and
+// j+1: a thread computes a run of stage-j outputs F in registers and emits
+// stage j+1's outputs as soon as their two F inputs exist, so F never goes
+// through HBM (reads 4R + 4 and writes 4R rows per run of R stage-j pairs,
+// instead of 6R + 4 and 6R).  Every output is the same sum in the same order
+// as the single-stage kernels: bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int kWavQP2 = 8;
+
+__global__ void __launch_bounds__(kWavBS) wav_syn_pairs2(const double *__restrict__ C,
+                                                         const double *__restrict__ Dm,
+                                                         const double *__restrict__ Dm2,
+                                                         double *__restrict__ Y, int j, double s,
+                                                         double s2, int64_t nx, ColMask msk)
+{
+    const int nw = 1 << (j - 1), nw2 = 1 << j;          // wavelets of levels j, j+1
+    const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
+    if (i >= nx) return;
+    const int q0 = blockIdx.y * kWavQP2;
+    const int q1 = min(q0 + kWavQP2, nw + 1);            // stage-j pairs [q0, q1)
+    const int f0 = 2 * q0, f1 = min(2 * q1, 2 * nw + 1); // F rows this thread emits G for
+    if (msk(i)) {
+        for (int f = f0; f < f1; ++f) {
+            if (f < nw2) Y[(int64_t)(2 * f + 1) * nx + i] = 0.0;
+            Y[(int64_t)(2 * f) * nx + i] = 0.0;
+        }
+        return;
+    }
+    auto Cr = [&](int q) { return C[(int64_t)q * nx + i]; };
+    auto D1 = [&](int k) { return Dm[(int64_t)k * nx + i]; };
+    auto D2 = [&](int k) { return Dm2[(int64_t)k * nx + i]; };
+    // F[2q] and F[2q+1] of stage j (wav_syn_pairs' arithmetic)
+    auto Feven = [&](int q, double cq, double dm, double dq) {
+        double acc = cq;
+        if (q >= 1) acc = add_rn(acc, mul_rn(qb(s, q - 1, nw), dm));
+        if (q < nw) acc = add_rn(acc, mul_rn(qa(s, q), dq));
+        return acc;
+    };
+    auto Fodd = [&](double cq, double cn, double dq) {
+        double od = mul_rn(0.5, cq);
+        od = add_rn(od, mul_rn(0.5, cn));
+        return add_rn(od, mul_rn(s, dq));
+    };
+    // G[2f], G[2f+1] of stage j+1 from F[f], F[f+1] (F[f+1] unused if f == nw2)
+    double gdm = f0 >= 1 ? D2(f0 - 1) : 0.0;              // d2[f-1]
+    auto emit = [&](int f, double Ff, double Fn) {
+        double acc = Ff;
+        if (f >= 1) acc = add_rn(acc, mul_rn(qb(s2, f - 1, nw2), gdm));
+        if (f < nw2) {
+            const double dq = D2(f);
+            acc = add_rn(acc, mul_rn(qa(s2, f), dq));
+            double od = mul_rn(0.5, Ff);
+            od = add_rn(od, mul_rn(0.5, Fn));
+            od = add_rn(od, mul_rn(s2, dq));
+            Y[(int64_t)(2 * f + 1) * nx + i] = od;
+            gdm = dq;
+        }
+        Y[(int64_t)(2 * f) * nx + i] = acc;
+    };
+    double cq = Cr(q0);
+    double dm = q0 >= 1 ? D1(q0 - 1) : 0.0;
+    double Fprev = 0.0;                                   // F[f-1], pending emission
+    bool pending = false;
+    for (int q = q0; q < q1; ++q) {
+        const double dq = q < nw ? D1(q) : 0.0;
+        const double fe = Feven(q, cq, dm, dq);           // F[2q]
+        if (pending) emit(2 * q - 1, Fprev, fe);
+        if (q < nw) {
+            const double cn = Cr(q + 1);
+            const double fo = Fodd(cq, cn, dq);           // F[2q+1]
+            emit(2 * q, fe, fo);
+            Fprev = fo;
+            pending = true;
+            cq = cn;
+            dm = dq;
+        } else {
+            emit(2 * q, fe, 0.0);                         // F[2 nw] = the last fine node
+            pending = false;
+        }
+    }
+    if (pending) {                                        // F[2 q1 - 1] needs F[2 q1]
+        const double dq = q1 < nw ? D1(q1) : 0.0;
+        emit(2 * q1 - 1, Fprev, Feven(q1, cq, dm, dq));
+    }
+}
+
+// transposed stages j+1 and j in one pass: a thread owns stage-j outputs
+// r in [r0, r1) (coarse C and wavelet d_j), computes the stage-(j+1) coarse
+// values F it needs from the fine rows X in registers, and writes the
+// stage-(j+1) wavelets d_{j+1} of F rows [2 r0, 2 r1) (wav_ana_pairs'
+// arithmetic throughout: bit-identical)
+__global__ void __launch_bounds__(kWavBS) wav_ana_pairs2(const double *__restrict__ X,
+                                                         double *__restrict__ Cout,
+                                                         double *__restrict__ Dout,
+                                                         double *__restrict__ Dout2, int j,
+                                                         double s, double s2, int64_t nx,
+                                                         ColMask msk)
+{
+    const int nw = 1 << (j - 1), nf = (1 << j) + 1;      // stage j: fine prefix F of nf rows
+    const int nw2 = 1 << j, nf2 = (1 << (j + 1)) + 1;    // stage j+1: fine prefix X of nf2 rows
+    const int64_t i = (int64_t)blockIdx.x * kWavBS + threadIdx.x;
+    if (i >= nx) return;
+    const int r0 = blockIdx.y * kWavQP2;
+    const int r1 = min(r0 + kWavQP2, nw + 1);
+    const int f0 = 2 * r0, f1 = min(2 * r1, nf);         // d_{j+1} rows this thread writes
+    if (msk(i)) {
+        for (int f = f0; f < f1; ++f)
+            if (2 * f + 1 < nf2) Dout2[(int64_t)f * nx + i] = 0.0;
+        for (int r = r0; r < r1; ++r) {
+            if (2 * r + 1 < nf) Dout[(int64_t)r * nx + i] = 0.0;
+            Cout[(int64_t)r * nx + i] = 0.0;
+        }
+        return;
+    }
+    auto Xr = [&](int k) { return X[(int64_t)k * nx + i]; };
+    // stage j+1 at F row f: coarse F[f] and (f < nw2, if write) wavelet
+    // d2[f], from x[2f-1 .. 2f+2] (wav_ana_pairs' arithmetic)
+    auto stage2 = [&](int f, double xm, double x0, double x1, double x2, bool write) {
+        double acc;
+        if (f >= 1) {
+            acc = mul_rn(0.5, xm);
+            acc = add_rn(acc, x0);
+        } else {
+            acc = x0;
+        }
+        if (2 * f + 1 < nf2) {
+            acc = add_rn(acc, mul_rn(0.5, x1));
+            if (write) {
+                double dd = mul_rn(qa(s2, f), x0);
+                dd = add_rn(dd, mul_rn(s2, x1));
+                dd = add_rn(dd, mul_rn(qb(s2, f, nw2), x2));
+                Dout2[(int64_t)f * nx + i] = dd;
+            }
+        }
+        return acc;
+    };
+    // F[f] for f in [fs, fe], fs = 2 r0 - 1 (F[2 r0 - 1] is recomputed; its
+    // wavelet belongs to the previous run), each x row read once
+    constexpr int NFV = 2 * kWavQP2 + 2;
+    const int fs = 2 * r0 - 1;
+    const int fb = fs < 0 ? 0 : fs;
+    const int fe = min(2 * r1, nw2);
+    double F[NFV];
+    double xa = fb >= 1 ? Xr(2 * fb - 1) : 0.0, xb = Xr(2 * fb);
+#pragma unroll
+    for (int t = 0; t < NFV; ++t) {
+        const int f = fs + t;
+        F[t] = 0.0;
+        if (f < fb || f > fe) continue;
+        double xc = 0.0, xd = 0.0;
+        if (2 * f + 1 < nf2) {
+            xc = Xr(2 * f + 1);
+            xd = Xr(2 * f + 2);
+        }
+        F[t] = stage2(f, xa, xb, xc, xd, f >= f0 && f < f1);
+        xa = xc;
+        xb = xd;
+    }
+    // stage j (wav_ana_pairs on F): C[r], d_j[r]
+#pragma unroll
+    for (int u = 0; u < kWavQP2; ++u) {
+        const int r = r0 + u;
+        if (r >= r1) break;
+        const int t = 2 * u + 1;                          // F[2r] = F[t]
+        double acc;
+        if (r >= 1) {
+            acc = mul_rn(0.5, F[t - 1]);
+            acc = add_rn(acc, F[t]);
+        } else {
+            acc = F[t];
+        }
+        if (2 * r + 1 < nf) {
+            acc = add_rn(acc, mul_rn(0.5, F[t + 1]));
+            double dd = mul_rn(qa(s, r), F[t]);
+            dd = add_rn(dd, mul_rn(s, F[t + 1]));
+            dd = add_rn(dd, mul_rn(qb(s, r, nw), F[t + 2]));
+            Dout[(int64_t)r * nx + i] = dd;
         }
         Cout[(int64_t)r * nx + i] = acc;
     }
@@ -258,6 +443,17 @@ cudaError_t launch_ana_stage(int j, double s, const double *X, int64_t x0, doubl
     return cudaGetLastError();
 }
 
+// A/B switch (HWG_WAV_FUSE=0: one launch per stage)
+static bool wavelet_fuse_enabled()
+{
+    static int on = -1;
+    if (on < 0) {
+        const char *ev = getenv("HWG_WAV_FUSE");
+        on = (ev && ev[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
+
 // Y = W X (transpose = 0) or W^T X (transpose = 1).  S1 (and S2 for the
 // transpose) are scratch arrays with at least 2^(J-1)+1 rows.
 cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, int J,
@@ -269,10 +465,14 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
         return cudaMemcpyAsync(Y, X, (size_t)(nt * nx) * sizeof(double),
                                cudaMemcpyDeviceToDevice, st);
     }
+    // the top two stages run fused (wav_*_pairs2); J = 1 has one stage
+    const bool fuse = J >= 2 && wavelet_fuse_enabled();
     if (!transpose) {
         const double *src = X;
-        for (int j = 1; j <= J; ++j) {
-            double *dst = ((J - j) % 2 == 0) ? Y : S1;
+        const int jlast = fuse ? J - 2 : J;              // single stages 1..jlast
+        for (int j = 1; j <= jlast; ++j) {
+            double *dst = ((jlast - j) % 2 == 0) ? (fuse ? S1 : Y) : (fuse ? Y : S1);
+            if (!fuse) dst = ((J - j) % 2 == 0) ? Y : S1;
             const int64_t nc = (1LL << (j - 1)) + 1;
             wav_syn_pairs<<<pair_grid((1 << (j - 1)) + 1, nx), kWavBS, 0, st>>>(
                 src, X + nc * nx, dst, j, scale[j - 1], nx, msk);
@@ -281,10 +481,36 @@ cudaError_t wavelet_apply(const double *X, double *Y, double *S1, double *S2, in
             ++*launches;
             src = dst;
         }
+        if (fuse) {
+            const int j = J - 1;                          // stages J-1 and J
+            const int64_t nc = (1LL << (j - 1)) + 1, nc2 = (1LL << j) + 1;
+            const dim3 g((unsigned)((nx + kWavBS - 1) / kWavBS),
+                         (unsigned)(((1 << (j - 1)) + 1 + kWavQP2 - 1) / kWavQP2));
+            wav_syn_pairs2<<<g, kWavBS, 0, st>>>(j == 1 ? X : src, X + nc * nx, X + nc2 * nx, Y, j,
+                                                 scale[j - 1], scale[j], nx, msk);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            ++*launches;
+        }
     } else {
         const double *src = X;
-        for (int j = J; j >= 1; --j) {
-            double *cdst = (j == 1) ? Y : (((J - j) % 2 == 0) ? S1 : S2);
+        int jtop = J;
+        if (fuse) {                                       // stages J and J-1
+            const int j = J - 1;
+            const int64_t nc = (1LL << (j - 1)) + 1, nc2 = (1LL << j) + 1;
+            double *cdst = (j == 1) ? Y : S1;
+            const dim3 g((unsigned)((nx + kWavBS - 1) / kWavBS),
+                         (unsigned)(((1 << (j - 1)) + 1 + kWavQP2 - 1) / kWavQP2));
+            wav_ana_pairs2<<<g, kWavBS, 0, st>>>(X, cdst, Y + nc * nx, Y + nc2 * nx, j,
+                                                 scale[j - 1], scale[j], nx, msk);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            ++*launches;
+            src = cdst;
+            jtop = J - 2;
+        }
+        for (int j = jtop; j >= 1; --j) {
+            double *cdst = (j == 1) ? Y : (((jtop - j) % 2 == 0) ? (fuse ? S2 : S1) : (fuse ? S1 : S2));
             const int64_t nc = (1LL << (j - 1)) + 1;
             wav_ana_pairs<<<pair_grid((1 << (j - 1)) + 1, nx), kWavBS, 0, st>>>(
                 src, cdst, Y + nc * nx, j, scale[j - 1], nx, msk);
