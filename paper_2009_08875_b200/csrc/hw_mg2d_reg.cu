@@ -495,6 +495,24 @@ struct RegPass {
         }
     }
 
+    // the first sweep of a zero-start DOWN pass: the old rows (right and
+    // below) are zero, so only the new row above and the left neighbour
+    // remain (3 FP64 operations per point instead of 6)
+    HW_DEV void chunk_zs(const double u[P], double uL, const double b[P], double y[P],
+                         unsigned rm) const
+    {
+        double yy = 0.0;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const double ul = k ? u[k - 1] : uL;
+            double pv = fma(-cxs, u[k], b[k]);
+            if constexpr (DG) pv = fma(-cds, ul, pv);
+            yy = fma(beta, yy, pv);
+            if (LSH && ((rm >> k) & 1u)) yy = 0.0;
+            y[k] = yy;
+        }
+    }
+
     HW_DEV double wscan(double s) const
     {
 #pragma unroll
@@ -527,11 +545,8 @@ struct RegPass {
         constexpr int LBr = LB0 ^ PAR, LXr = LX0 ^ PAR ^ 1;   // UP parities of b(t), x0(t+1)
         double dn0[P + 1];
         if constexpr (DOWN && ZS) {
-            double z[P];
-#pragma unroll
-            for (int k = 0; k < P; ++k) z[k] = 0.0;
             load_b<LBr>(0, b);
-            chunk(X1[Q], X1L, z, 0.0, z, 0.0, b, y[0], rm0);
+            chunk_zs(X1[Q], X1L, b, y[0], rm0);
         } else {
             load_x0<Q, EDGE, LXr>(t + 1, sx, sc, dn0);
             load_b<LBr>(0, b);

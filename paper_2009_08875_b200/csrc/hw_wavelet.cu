@@ -197,7 +197,10 @@ __global__ void __launch_bounds__(kWavBS) wav_syn_pairs2(const double *__restric
     double dm = q0 >= 1 ? D1(q0 - 1) : 0.0;
     double Fprev = 0.0;                                   // F[f-1], pending emission
     bool pending = false;
-    for (int q = q0; q < q1; ++q) {
+#pragma unroll
+    for (int u = 0; u < kWavQP2; ++u) {
+        const int q = q0 + u;
+        if (q >= q1) break;
         const double dq = q < nw ? D1(q) : 0.0;
         const double fe = Feven(q, cq, dm, dq);           // F[2q]
         if (pending) emit(2 * q - 1, Fprev, fe);
