@@ -11,9 +11,10 @@ Fixtures (tests/golden/make_golden.py, generated here from the REFERENCE):
 These store 65,536 seeded sample positions of f-hat, w, u (the arrays are
 0.1-0.5 GB) plus norms and the full residual / CG-scalar histories.
 
-cfg4full -- BASELINE cfg 4 itself (1.07e9 dofs), solved by the CPU oracle at
-full size on the GPU box's host (scripts/oracle_full_run.py; the oracle is
-pinned bit-exact to the reference's fixtures, and to c410 here).
+cfg4full / cfg3full -- BASELINE cfg 4 and cfg 3 themselves (1.07e9 dofs
+each), solved by the CPU oracle at full size on the GPU box's host
+(scripts/oracle_full_run.py; the oracle is pinned bit-exact to the
+reference's fixtures, and to c410 here).
 
 Bar (BASELINE north_star): identical iteration count, u within 1e-8
 relative l2; multigrid rows within 1e-12 (max-abs relative, as
@@ -112,22 +113,23 @@ def test_c410_full_arrays_against_oracle():
     assert _rel_l2(u.cpu().numpy(), uo) <= 1e-8
 
 
-@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "cfg4full.json")),
-                    reason="full-size oracle fixture not generated")
-def test_bench_config_cfg4_against_full_oracle_run():
-    """BASELINE cfg 4 (J = 10, K = 10, 1.07e9 dofs) -- the benched workload --
-    against the oracle's full-size solve (scripts/oracle_full_run.py): same
-    iteration count and residual history, f-hat / w / u at 65,536 seeded
-    positions and their norms within 1e-8.  The same script compared the
-    FULL arrays when it ran (recorded in cfg4full.json: gpu_comparison)."""
+@pytest.mark.parametrize("name", ["cfg4full", "cfg3full"])
+def test_bench_config_against_full_oracle_run(name):
+    """BASELINE cfg 4 (J = 10, K = 10) and cfg 3 (1D J = 20, K = 10), 1.07e9
+    dofs each -- the benched workloads -- against the oracle's full-size
+    solve on the GPU box's host (scripts/oracle_full_run.py): same iteration
+    count and residual history, f-hat / w / u at 65,536 seeded positions and
+    their norms within 1e-8.  The same script compared the FULL arrays when
+    it ran (recorded in <name>.json: gpu_comparison)."""
+    if not os.path.exists(os.path.join(GOLDEN, f"{name}.json")):
+        pytest.skip(f"full-size oracle fixture {name} not generated")
     gc.collect()
     torch.cuda.empty_cache()
-    meta, g = golden("cfg4full")
+    meta, g = golden(name)
     rec = meta.get("gpu_comparison", {})
     if rec:
         assert rec["gpu_iterations"] == meta["iterations"]
         assert rec["rel_l2_u_full"] <= 1e-8 and rec["rel_l2_w_full"] <= 1e-8
-    meta = dict(meta, u0="sines")
     asm, res, u = _solve(meta)
     _check_against(meta, g, asm, res, u)
     del asm, res, u
