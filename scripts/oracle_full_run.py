@@ -136,14 +136,20 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--out", default="gpurun_out/cfg4full")
     ap.add_argument("--no-gpu", action="store_true")
+    ap.add_argument("--J", type=int, default=None, help="override J (cfg 5: the per-GPU share)")
     args = ap.parse_args()
     d, J, K, dist, u0 = inputs.recipe(args.config)
+    if args.J is not None:
+        J = args.J
+    domain = inputs.CONFIGS[args.config].get("domain", "square")
+    D = 0.25 * np.eye(2) if domain == "L" else None       # the mapped L (discretization.lshape_problem)
     t0 = time.time()
-    ref = oracle_solve(d, J, K, dist, u0)
+    ref = oracle_solve(d, J, K, dist, u0, D=D, domain=domain)
     n_t, n_x = ref["f"].shape
     log(f"oracle done: {ref['its']} iterations, {ref['seconds']:.0f} s")
     idx = np.sort(np.random.default_rng(SAMPLE_SEED).choice(n_t * n_x, min(NSAMPLE, n_t * n_x), replace=False))
     meta = dict(name=os.path.basename(args.out), config=args.config, d=d, J=J, K=K, dist=dist,
+                domain=domain, D=(np.eye(d) if D is None else D).tolist(),
                 n_t=n_t, n_x=n_x, seed_f=inputs.SEED_F, sample_seed=SAMPLE_SEED,
                 iterations=ref["its"], eps=ref["eps"], rho0=ref["rho0"],
                 residual_norms=ref["hist"], cg_alphas=ref["alphas"], cg_betas=ref["betas"],
@@ -159,7 +165,7 @@ def main():
     with open(args.out + ".json", "w") as fh:
         json.dump(meta, fh, indent=1)
     if not args.no_gpu:
-        cmp = gpu_solve_and_compare(args.config, d, J, K, dist, u0, ref)
+        cmp = gpu_solve_and_compare(args.config, d, J, K, dist, u0, ref, D=D, domain=domain)
         meta["gpu_comparison"] = cmp
         log(f"gpu: {cmp}")
         with open(args.out + ".json", "w") as fh:

@@ -63,8 +63,10 @@ def _solve(meta):
     d = meta["d"]
     u0 = inputs.u0_by_name(meta["u0"]) if "u0" in meta else inputs.u0_for(meta["dist"])
     F = inputs.forcing(meta["dist"], meta["n_t"], meta["n_x"])
-    asm = hw.assemble_system(hw.ProblemData(D=np.eye(d), c=0.0, u0=u0), meta["J"], meta["K"],
-                             hw.SolveConfig(), forcing=F, host_rhs=False)
+    D = np.asarray(meta["D"]) if "D" in meta else np.eye(d)
+    asm = hw.assemble_system(hw.ProblemData(D=D, c=0.0, u0=u0), meta["J"], meta["K"],
+                             hw.SolveConfig(), forcing=F, host_rhs=False,
+                             domain=meta.get("domain", "square"))
     del F
     res = hw.pcg(asm.S, asm.K_X, asm.rhs, 0.0, rtol=1e-6)
     u = asm.wavelet.apply_array(res.w.array)
@@ -113,10 +115,11 @@ def test_c410_full_arrays_against_oracle():
     assert _rel_l2(u.cpu().numpy(), uo) <= 1e-8
 
 
-@pytest.mark.parametrize("name", ["cfg4full", "cfg3full"])
+@pytest.mark.parametrize("name", ["cfg4full", "cfg3full", "cfg5share"])
 def test_bench_config_against_full_oracle_run(name):
     """BASELINE cfg 4 (J = 10, K = 10) and cfg 3 (1D J = 20, K = 10), 1.07e9
-    dofs each -- the benched workloads -- against the oracle's full-size
+    dofs each, and cfg 5's per-GPU share (mapped L, J = 8, K = 11, 8.1e8
+    dofs) -- the benched workloads -- against the oracle's full-size
     solve on the GPU box's host (scripts/oracle_full_run.py): same iteration
     count and residual history, f-hat / w / u at 65,536 seeded positions and
     their norms within 1e-8.  The same script compared the FULL arrays when
