@@ -199,3 +199,46 @@ def test_pcg_under_plan_matches_serial(small2d):
     b = hw.pcg(small2d.S, small2d.K_X, small2d.rhs, 1e-6, plan)
     assert a.residual_norms == b.residual_norms
     assert np.array_equal(a.w.array, b.w.array)
+
+
+# ---- test_wavelet.py: the transform on the GPU ------------------------------
+def _wavelet_ctx(J, cols):
+    from paper_2009_08875_b200.device import GpuContext
+    K = {1: 1, 3: 2}[cols]                       # 1D grids of 2^K - 1 = cols columns
+    return hw.WaveletTransform(GpuContext(1, J, K))
+
+
+def test_wavelet_matches_dense_recursion(rng):          # test_wavelet.py:69-76
+    from paper_2009_08875_b200 import structures as st
+    for J in range(1, 7):
+        wt = _wavelet_ctx(J, 3)
+        W = st.dense_transform(hw.build_wavelet(J))
+        X = rng.standard_normal((2 ** J + 1, 3))
+        assert relative_diff(wt.apply_array(X), W @ X) <= 1e-13
+        assert relative_diff(wt.transpose_apply_array(X), W.T @ X) <= 1e-13
+
+
+def test_wavelet_coarse_block_interpolates():           # test_wavelet.py:78-87
+    J = 4
+    wt = _wavelet_ctx(J, 1)
+    X = np.zeros((2 ** J + 1, 1))
+    X[0, 0], X[1, 0] = 1.0, 3.0
+    out = wt.apply_array(X)[:, 0]
+    nodes = np.linspace(0, 1, 2 ** J + 1)
+    assert np.abs(out - (1.0 + 2.0 * nodes)).max() <= 1e-14
+
+
+def test_wavelet_adjoint_identity(rng):                 # test_wavelet.py:89-96
+    wt = _wavelet_ctx(5, 1)
+    for _ in range(20):
+        x = rng.standard_normal((33, 1))
+        y = rng.standard_normal((33, 1))
+        lhs = (wt.apply_array(x) * y).sum()
+        rhs = (x * wt.transpose_apply_array(y)).sum()
+        assert abs(lhs - rhs) <= 1e-13 * max(abs(lhs), 1.0)
+
+
+def test_wavelet_shape_mismatch():                      # test_wavelet.py:60-66
+    wt = _wavelet_ctx(3, 1)
+    with pytest.raises(ValueError):
+        wt.apply_array(np.zeros((8, 1)))
