@@ -59,6 +59,9 @@ struct hwg_ctx {
     int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
     double *cmat1d = nullptr;           // 1D, K >= 6: [op][15][15] level-4 V-cycle operators
     int mg1d_dense = 1;                 // HWG_MG1D_DENSE=0: the level-4..1 sub-cycle (A/B)
+    int mg1d_rr = 0;                    // 1D, 7 <= K <= 10, |beta| <= 1/2: mg1d_rr
+    int mg1d_rr_minb = 3;               // HWG_RR_MINB=2: 8 warps/SM at 255 registers (A/B)
+    double *cmat_rr = nullptr;          // [op][63][64] level-6 V-cycle operators (mg1d_rr)
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
     int form = 0;                      // S: 0 five-term (Lemma 2), 1 test-space (Lemma 1)
@@ -348,8 +351,10 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
         const int32_t *ro = row_op ? row_op + r0 : nullptr;
         if (c->dim == 1) {
             Mg1dArgs a{Bp, c->nx, Xp, c->nx, c->coef, c->K + 1, c->K, c->nv, ro, op, nr, c->cmat1d};
+            a.cmat_rr = c->cmat_rr;
+            a.rr_minb = c->mg1d_rr_minb;
             ProfScope ps(c, st, 5, 16.0 * nr * c->nx);
-            CK(mg1d_launch(a, st));
+            CK(c->mg1d_rr ? mg1d_rr_launch(a, st) : mg1d_launch(a, st));
             ++c->launches;
             continue;
         }
@@ -555,6 +560,32 @@ static int build_coarse_1d(hwg_ctx *c)
     return HWG_OK;
 }
 
+// mg1d_rr: the V-cycle from level kRrCut (zero start) of every operator,
+// G[op][s][j] = (MG e_s)_j (rows padded to kRrCutLd with zero columns), run
+// by the exact shared-memory kernel on unit right-hand sides
+static int build_coarse_rr(hwg_ctx *c)
+{
+    const int nops = c->J + 2, n = kRrCutN;
+    const int64_t rows = (int64_t)nops * n;
+    std::vector<double> eye((size_t)rows * n, 0.0);
+    std::vector<int32_t> ops(rows);
+    for (int o = 0; o < nops; ++o)
+        for (int i = 0; i < n; ++i) {
+            eye[((size_t)o * n + i) * n + i] = 1.0;
+            ops[o * n + i] = o;
+        }
+    double *B = nullptr;
+    int32_t *dops = nullptr;
+    TRY(upload(c, &B, eye));
+    TRY(upload(c, &dops, ops));
+    TRY(dalloc(c, &c->cmat_rr, rows * kRrCutLd));
+    CK(cudaMemset(c->cmat_rr, 0, sizeof(double) * rows * kRrCutLd));
+    Mg1dArgs a{B, n, c->cmat_rr, kRrCutLd, c->coef, c->K + 1, kRrCut, 1, dops, 0, rows, nullptr};
+    CK(mg1d_launch(a, 0));
+    CK(cudaDeviceSynchronize());
+    return HWG_OK;
+}
+
 static int ensure_pcg(hwg_ctx *c)
 {
     if (c->r) return HWG_OK;
@@ -636,6 +667,20 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
         if (ev[0] == '1') c->coarse_fast = 0;
     if (const char *ev = getenv("HWG_MG1D_DENSE"))          // A/B switch for measurements
         if (ev[0] == '0') c->mg1d_dense = 0;
+    // 1D register-resident hierarchy: its truncated lane carries need |beta| <= 1/2
+    // on every level (always true for alpha A + mu M, alpha > 0, mu >= 0)
+    if (d.dim == 1 && d.K >= kRrCut + 1 && d.K <= 10) {
+        c->mg1d_rr = 1;
+        for (int op = 0; op < nops; ++op)
+            for (int l = kRrCut + 1; l <= d.K; ++l) {
+                const double *cf = &c->coef_host[((size_t)op * (d.K + 1) + l) * HWG_COEF_STRIDE];
+                if (!(fabs(cf[kCy] * cf[kInv]) <= 0.5)) c->mg1d_rr = 0;
+            }
+    }
+    if (const char *ev = getenv("HWG_MG1D"))                // A/B: 1 = mg1d_reg
+        if (ev[0] == '1') c->mg1d_rr = 0;
+    if (const char *ev = getenv("HWG_RR_MINB"))
+        if (ev[0] == '2') c->mg1d_rr_minb = 2;
     if (const char *ev = getenv("HWG_GRAPH"))               // A/B switch for measurements
         if (ev[0] == '0') c->use_graph = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask
@@ -666,6 +711,7 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     GO(upload(c, &c->row_op_kx, ops));
     GO(build_temporal(c));
     if (d.dim == 1 && d.K > kMg1dCut + 1) GO(build_coarse_1d(c));
+    if (c->mg1d_rr) GO(build_coarse_rr(c));
     if (!c->kernel_only) {
         GO(dalloc(c, &c->U, c->N));
         GO(dalloc(c, &c->MxU, c->N));

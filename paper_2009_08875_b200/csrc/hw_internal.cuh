@@ -68,10 +68,20 @@ struct Mg1dArgs {
     // this kernel with K = 4 on unit rows); mg1d_reg applies it instead of
     // the level-4..1 sub-cycle
     const double *cmat = nullptr;
+    // mg1d_rr: [op][kRrCutN][64] the V-cycle from level kRrCut (zero start),
+    // G[op][s][j] = (MG e_s)_j, columns padded to 64 with zeros
+    const double *cmat_rr = nullptr;
+    int rr_minb = 3;                              // mg1d_rr CTAs (4 warps) per SM
 };
 constexpr int kMg1dCut = 4;                    // levels <= kMg1dCut: dense operator
 constexpr int kMg1dCutN = (1 << kMg1dCut) - 1;  // 15
 cudaError_t mg1d_launch(const Mg1dArgs &a, cudaStream_t st);
+// register-resident hierarchy (hw_mg1d_rr.cu), 7 <= K <= 10, |beta| <= 1/2 on
+// every level; cudaErrorNotSupported otherwise
+constexpr int kRrCut = 6;                      // levels <= kRrCut: dense operator
+constexpr int kRrCutN = (1 << kRrCut) - 1;     // 63
+constexpr int kRrCutLd = 64;                   // padded row of the dense operator
+cudaError_t mg1d_rr_launch(const Mg1dArgs &a, cudaStream_t st);
 
 
 // ---- hw_wavelet.cu -------------------------------------------------------
