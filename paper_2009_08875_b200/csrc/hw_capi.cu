@@ -60,7 +60,7 @@ struct hwg_ctx {
     double *cmat1d = nullptr;           // 1D, K >= 6: [op][15][15] level-4 V-cycle operators
     int mg1d_dense = 1;                 // HWG_MG1D_DENSE=0: the level-4..1 sub-cycle (A/B)
     int mg1d_rr = 0;                    // 1D, 7 <= K <= 10, |beta| <= 1/2: mg1d_rr
-    int mg1d_rr_minb = 3;               // HWG_RR_MINB=2: 8 warps/SM at 255 registers (A/B)
+    int mg1d_rr_minb = 1;               // 1: persistent mg1d_rrp; HWG_RR_MINB=3 / 2: mg1d_rr (A/B)
     double *cmat_rr = nullptr;          // [op][63][64] level-6 V-cycle operators (mg1d_rr)
     int64_t nt = 0, nx = 0, N = 0;     // N = nt * nx (nx: grid points per row)
     int domain = 0;                    // 1: L-shaped (embedded grid, masked quadrant)
@@ -680,7 +680,7 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     if (const char *ev = getenv("HWG_MG1D"))                // A/B: 1 = mg1d_reg
         if (ev[0] == '1') c->mg1d_rr = 0;
     if (const char *ev = getenv("HWG_RR_MINB"))
-        if (ev[0] == '2') c->mg1d_rr_minb = 2;
+        if (ev[0] == '2' || ev[0] == '3') c->mg1d_rr_minb = ev[0] - '0';
     if (const char *ev = getenv("HWG_GRAPH"))               // A/B switch for measurements
         if (ev[0] == '0') c->use_graph = 0;
     // streamed levels without mg2d_reg: mg2d_stream covers n <= 1023 and has no mask

@@ -50,6 +50,10 @@ cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, c
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
 // largest |beta| = |cy / c0| mg2d_reg accepts (8-chunk window: |beta|^32 <= 2^-60)
 constexpr double kRegBetaMax = 0.2726;
+// batches of at most kWideRows temporal rows run levels in kWideLevels (bit l)
+// with more threads per row (mg2d_reg_launch)
+constexpr int64_t kWideRows = 0;
+constexpr int kWideLevels = 0;
 cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st);
 
 // ---- hw_mg1d.cu ----------------------------------------------------------
@@ -71,7 +75,7 @@ struct Mg1dArgs {
     // mg1d_rr: [op][kRrCutN][64] the V-cycle from level kRrCut (zero start),
     // G[op][s][j] = (MG e_s)_j, columns padded to 64 with zeros
     const double *cmat_rr = nullptr;
-    int rr_minb = 3;                              // mg1d_rr CTAs (4 warps) per SM
+    int rr_minb = 1;                              // 1: mg1d_rrp; 3 / 2: mg1d_rr CTAs (4 warps) per SM
 };
 constexpr int kMg1dCut = 4;                    // levels <= kMg1dCut: dense operator
 constexpr int kMg1dCutN = (1 << kMg1dCut) - 1;  // 15

@@ -225,21 +225,28 @@ HW_DEV void prolongate(double (&x)[RL<L>::C], const double (&xc)[RL<L>::C / 2], 
     if (lane == 31) x[C - 1] = 0.0;
 }
 
-// x (level kRrCut, C = 2 points per lane) = G b: b broadcast from shared memory
+// x (level kRrCut, C = 2 points per lane) = G b: b broadcast from shared
+// memory; GS: G staged in shared memory by the CTA (mg1d_rrp), else read
+// through L1
+template <bool GS>
 HW_DEV void dense_cut(double (&x)[RL<kRrCut>::C], const double *s, const double *G, int lane)
 {
     constexpr int C = RL<kRrCut>::C, n = (1 << kRrCut) - 1, ld = 32 * C;
     static_assert(C == 2, "dense_cut assumes two points per lane at the cut level");
     double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
     const double *g = G + 2 * lane;
+    auto ldg2 = [](const double *p) {
+        if constexpr (GS) return *reinterpret_cast<const double2 *>(p);
+        else return __ldg(reinterpret_cast<const double2 *>(p));
+    };
 #pragma unroll 8
     for (int m = 0; m < (n + 1) / 2; ++m) {           // points 2m, 2m+1 (unit m, no swizzle at U = 1)
         const double2 bb = *reinterpret_cast<const double2 *>(s + RL<kRrCut>::off + 2 * m);
-        const double2 g0 = __ldg(reinterpret_cast<const double2 *>(g + (2 * m) * ld));
+        const double2 g0 = ldg2(g + (2 * m) * ld);
         a0 = fma(g0.x, bb.x, a0);
         a1 = fma(g0.y, bb.x, a1);
         if (2 * m + 1 < n) {
-            const double2 g1 = __ldg(reinterpret_cast<const double2 *>(g + (2 * m + 1) * ld));
+            const double2 g1 = ldg2(g + (2 * m + 1) * ld);
             c0 = fma(g1.x, bb.y, c0);
             c1 = fma(g1.y, bb.y, c1);
         }
@@ -261,7 +268,7 @@ HW_DEV Lv level_coef(const double *coef, int L)
     return v;
 }
 
-template <int L, bool TOP>
+template <int L, bool TOP, bool GS>
 HW_DEV void vcycle(double (&x)[RL<L>::C], double *s, const double *coef, const double *G,
                    int lane, bool zs)
 {
@@ -275,9 +282,9 @@ HW_DEV void vcycle(double (&x)[RL<L>::C], double *s, const double *coef, const d
     __syncwarp();
     double xc[C / 2];
     if constexpr (L - 1 == kRrCut) {
-        dense_cut(xc, s, G, lane);
+        dense_cut<GS>(xc, s, G, lane);
     } else {
-        vcycle<L - 1, false>(xc, s, coef, G, lane, true);
+        vcycle<L - 1, false, GS>(xc, s, coef, G, lane, true);
     }
     prolongate<L>(x, xc, lane);
     sweep<L, false, false>(x, s, cf.beta, lane);
@@ -320,13 +327,94 @@ __global__ void __launch_bounds__(32 * WPB, MINB) mg1d_rr(Mg1dArgs a)
     double x[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) x[k] = 0.0;
-    for (int cyc = 0; cyc < a.ncyc; ++cyc) vcycle<K, true>(x, s, coef, G, lane, cyc == 0);
+    for (int cyc = 0; cyc < a.ncyc; ++cyc) vcycle<K, true, false>(x, s, coef, G, lane, cyc == 0);
     __syncwarp();
     store_b<K>(s, lane, x);                           // the row through the same slots
     __syncwarp();
     double *Xg = a.X + row * a.ldX;
 #pragma unroll 4
     for (int j = lane; j < nK; j += 32) Xg[j] = s[RL<K>::point(j)];
+}
+
+// mg1d_rrp: the same per-row work as mg1d_rr in one persistent CTA of WPB
+// warps per SM.  Rows are dealt out in tiles of WPB * TR consecutive rows;
+// the dense cut-level operator of a tile's (first row's) multigrid operator
+// is staged once in shared memory -- the rows of one wavelet level are
+// contiguous, so it changes J + 1 times over the whole batch -- and every
+// row of that operator applies it with LDS instead of 128 L1/L2 loads.  A row
+// with another operator (a tile that straddles two levels) reads it through
+// L1 as mg1d_rr does.  The row itself is loaded with 32 independent
+// streaming loads per lane; the warp's next row is prefetched into L2.
+template <int K, int WPB>
+__global__ void __launch_bounds__(32 * WPB, 1) mg1d_rrp(Mg1dArgs a, int TR)
+{
+    using namespace rr;
+    constexpr int C = RL<K>::C;
+    constexpr int words = RL<K>::off + RL<K>::size;
+    constexpr int gwords = kRrCutN * kRrCutLd;
+    constexpr int nK = (1 << K) - 1;
+    extern __shared__ double4 smraw[];
+    double *Gs = reinterpret_cast<double *>(smraw);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *s = Gs + kRrCutLd * kRrCutLd + (size_t)w * words;
+    const int64_t tile_rows = (int64_t)WPB * TR;
+    const int64_t ntiles = (a.rows + tile_rows - 1) / tile_rows;
+    int cur_op = -1;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row0 = tile * tile_rows;
+        const int op_t = a.row_op ? a.row_op[row0] : a.op;
+        if (op_t != cur_op) {                          // uniform over the CTA
+            __syncthreads();                           // nobody still reads the old operator
+            const double2 *src = reinterpret_cast<const double2 *>(a.cmat_rr + (int64_t)op_t * gwords);
+            double2 *dst = reinterpret_cast<double2 *>(Gs);
+            for (int q = threadIdx.x; q < gwords / 2; q += 32 * WPB) dst[q] = __ldg(src + q);
+            cur_op = op_t;
+            __syncthreads();
+        }
+        for (int i = 0; i < TR; ++i) {
+            const int64_t row = row0 + (int64_t)i * WPB + w;
+            if (row >= a.rows) break;
+            {   // the row this warp handles next, into L2
+                const int64_t nxt = i + 1 < TR ? row + WPB : row + (int64_t)gridDim.x * tile_rows - (int64_t)(TR - 1) * WPB;
+                if (nxt < a.rows) {
+                    const char *p = reinterpret_cast<const char *>(a.B + nxt * a.ldB);
+                    for (int o = lane * 128; o < nK * 8; o += 32 * 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + o));
+                }
+            }
+            const int op = a.row_op ? a.row_op[row] : a.op;
+            const double *coef = a.coef + (int64_t)op * a.levels_p1 * kCoefStride;
+            {   // b' = b / c0 of the finest level: all the lane's loads in flight at once
+                const double inv = coef[K * kCoefStride + kInv];
+                const double *Bg = a.B + row * a.ldB;
+                double v[C];
+#pragma unroll
+                for (int k = 0; k < C; ++k) {
+                    const int j = lane + 32 * k;
+                    v[k] = j < nK ? __ldcs(Bg + j) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < C; ++k) s[RL<K>::point(lane + 32 * k)] = v[k] * inv;
+                __syncwarp();
+            }
+            double x[C];
+#pragma unroll
+            for (int k = 0; k < C; ++k) x[k] = 0.0;
+            if (op == cur_op) {
+                for (int cyc = 0; cyc < a.ncyc; ++cyc) vcycle<K, true, true>(x, s, coef, Gs, lane, cyc == 0);
+            } else {
+                const double *G = a.cmat_rr + (int64_t)op * gwords;
+                for (int cyc = 0; cyc < a.ncyc; ++cyc) vcycle<K, true, false>(x, s, coef, G, lane, cyc == 0);
+            }
+            __syncwarp();
+            store_b<K>(s, lane, x);                       // the row through the same slots
+            __syncwarp();
+            double *Xg = a.X + row * a.ldX;
+#pragma unroll 8
+            for (int j = lane; j < nK; j += 32) __stcs(Xg + j, s[RL<K>::point(j)]);
+            __syncwarp();                                 // the slots are rewritten by the next row
+        }
+    }
 }
 
 template <int K, int MINB>
@@ -344,9 +432,39 @@ static cudaError_t launch_rr(const Mg1dArgs &a, cudaStream_t st)
     return cudaGetLastError();
 }
 
+template <int K>
+static cudaError_t launch_rrp(const Mg1dArgs &a, cudaStream_t st)
+{
+    constexpr int WPB = 12;
+    constexpr int words = rr::RL<K>::off + rr::RL<K>::size;
+    const size_t smem = ((size_t)kRrCutLd * kRrCutLd + (size_t)WPB * words) * sizeof(double);
+    auto k = mg1d_rrp<K, WPB>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // rows per warp and tile: at least ~16 tiles per SM (strided tiles, <= 6 % imbalance)
+    const int64_t per = a.rows / (148LL * WPB * 16);
+    const int TR = per < 1 ? 1 : (per > 8 ? 8 : (int)per);
+    const int64_t ntiles = (a.rows + (int64_t)WPB * TR - 1) / ((int64_t)WPB * TR);
+    const int64_t grid = ntiles < 148 ? ntiles : 148;
+    k<<<(unsigned)grid, 32 * WPB, smem, st>>>(a, TR);
+    return cudaGetLastError();
+}
+
 cudaError_t mg1d_rr_launch(const Mg1dArgs &a, cudaStream_t st)
 {
-    // minb = 3: 12 warps/SM at <= 168 registers; 2: 8 warps/SM at <= 255 (A/B)
+    if (a.rows <= 0) return cudaSuccess;
+    // rr_minb = 1 (default): the persistent kernel, 12 warps/SM, the cut-level
+    // operator in shared memory.  3: mg1d_rr, 12 warps/SM as 3 CTAs (A/B);
+    // 2: mg1d_rr at 8 warps/SM and <= 255 registers (A/B)
+    if (a.rr_minb == 1) {
+        switch (a.K) {
+        case 7: return launch_rrp<7>(a, st);
+        case 8: return launch_rrp<8>(a, st);
+        case 9: return launch_rrp<9>(a, st);
+        case 10: return launch_rrp<10>(a, st);
+        default: return cudaErrorNotSupported;
+        }
+    }
     if (a.rr_minb == 2) {
         switch (a.K) {
         case 7: return launch_rr<7, 2>(a, st);

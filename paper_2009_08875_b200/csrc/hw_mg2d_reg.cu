@@ -50,6 +50,7 @@
 #include "hw_internal.cuh"
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace hw {
 namespace {
@@ -772,19 +773,42 @@ cudaError_t launch_reg_n(const MgStreamArgs &a, bool down, int64_t rows, cudaStr
 
 }  // namespace
 
+// Thread shape per level.  The default shapes (P = 8 points per thread) are
+// the HBM-efficient ones for batches of a wave or more.  A batch below
+// kWideRows temporal rows leaves each SM with one or two warps of a level
+// <= 9 pass, each issuing a whole grid row's three sweeps alone; the WIDE
+// shapes split the row over 2-4x the threads (P = 4 / 2, the same 32-column
+// carry window).  HWG_REG_WIDE=<bitmask of levels> forces them (A/B), =0
+// disables them.
+static int wide_mask(int64_t rows)
+{
+    if (const char *ev = getenv("HWG_REG_WIDE")) return atoi(ev);   // read per launch (A/B)
+    return rows <= kWideRows ? kWideLevels : 0;
+}
+
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
+    const int wide = wide_mask(rows);
     switch (a.n) {
     case 63: return launch_reg_n<2, 32, 1>(a, down, rows, st);
-    case 127: return launch_reg_n<4, 32, 1>(a, down, rows, st);
-    case 255: return launch_reg_n<8, 32, 1>(a, down, rows, st);
-    case 511: return launch_reg_n<8, 64, 1>(a, down, rows, st);
+    case 127:
+        if (wide & (1 << 7)) return launch_reg_n<2, 64, 1>(a, down, rows, st);
+        return launch_reg_n<4, 32, 1>(a, down, rows, st);
+    case 255:
+        if (wide & (1 << 8)) return launch_reg_n<4, 64, 1>(a, down, rows, st);
+        if (wide & (1 << 18)) return launch_reg_n<2, 128, 1>(a, down, rows, st);
+        return launch_reg_n<8, 32, 1>(a, down, rows, st);
+    case 511:
+        if (wide & (1 << 9)) return launch_reg_n<4, 128, 1>(a, down, rows, st);
+        return launch_reg_n<8, 64, 1>(a, down, rows, st);
     case 1023:
         // HWG_MG_REG=4: P = 4 for both passes; =5: P = 4 for UP only (A/B)
-        if (a.reg_ok == 2 || (a.reg_ok == 3 && !down))
+        if (a.reg_ok == 2 || (a.reg_ok == 3 && !down) || (wide & (1 << 10)))
             return launch_reg_n<4, 256, 1>(a, down, rows, st);
         return launch_reg_n<8, 128, 2>(a, down, rows, st);
-    case 2047: return launch_reg_n<8, 256, 1>(a, down, rows, st);
+    case 2047:
+        if (wide & (1 << 11)) return launch_reg_n<4, 512, 1>(a, down, rows, st);
+        return launch_reg_n<8, 256, 1>(a, down, rows, st);
     default: return cudaErrorNotSupported;
     }
 }

@@ -3,7 +3,8 @@ batch (K = 10, 2^J + 1 rows, every row its own C_j operator).
 
     HWG_MG1D=1 python scripts/mg1d_ab.py [J]        # round-1/2 mg1d_reg (one warp, exact scans)
     HWG_RR_MINB=2 python scripts/mg1d_ab.py [J]     # mg1d_rr at 8 warps/SM (255 registers)
-    python scripts/mg1d_ab.py [J]                   # default (mg1d_rr, 12 warps/SM)
+    HWG_RR_MINB=3 python scripts/mg1d_ab.py [J]     # mg1d_rr, 12 warps/SM as 3 CTAs, operator through L1
+    python scripts/mg1d_ab.py [J]                   # default (persistent mg1d_rrp, operator in shared memory)
 """
 import os
 import sys
@@ -34,12 +35,12 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
-tag = "k" + os.environ.get("HWG_MG1D", "2") + "m" + os.environ.get("HWG_RR_MINB", "3")
+tag = "k" + os.environ.get("HWG_MG1D", "2") + "m" + os.environ.get("HWG_RR_MINB", "1")
 np.save(f"/tmp/mg1d_X_{tag}.npy", X[:64].cpu().numpy())
 print(f"HWG_MG1D={tag} J={J} rows={n_t}: {ms:.3f} ms per batch, {ms * 1e3 / n_t * 1e3:.1f} ns/row, "
       f"{16.0 * n_t * n_x / ms / 1e6:.1f} GB/s (b in, x out)")
-other = "/tmp/mg1d_X_k1m3.npy"
-if tag != "k1m3" and os.path.exists(other):
+other = "/tmp/mg1d_X_k1m1.npy"
+if tag != "k1m1" and os.path.exists(other):
     A = np.load(other)
     Bf = X[:64].cpu().numpy()
     print(f"{tag} vs mg1d_reg: max rel diff", float(np.abs(A - Bf).max() / np.abs(A).max()))
