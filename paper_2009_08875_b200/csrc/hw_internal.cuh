@@ -50,10 +50,9 @@ cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, c
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
 // largest |beta| = |cy / c0| mg2d_reg accepts (8-chunk window: |beta|^32 <= 2^-60)
 constexpr double kRegBetaMax = 0.2726;
-// batches of at most kWideRows temporal rows run levels in kWideLevels (bit l)
-// with more threads per row (mg2d_reg_launch)
-constexpr int64_t kWideRows = 0;
-constexpr int kWideLevels = 0;
+// mg2d_reg_launch: levels 7-9 switch to twice the threads per row while the
+// batch has at most kWideWarps default-shape warps (~2 per SM)
+constexpr int64_t kWideWarps = 320;
 cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st);
 
 // ---- hw_mg1d.cu ----------------------------------------------------------

@@ -46,7 +46,12 @@ def _sampled(t, idx):
     return t.reshape(-1)[torch.from_numpy(idx).to(t.device)].cpu().numpy()
 
 
-def test_multigrid_K10_rows_match_reference():
+@pytest.mark.parametrize("shapes", ["auto", "p8"])
+def test_multigrid_K10_rows_match_reference(shapes, monkeypatch):
+    # "p8": the default thread shapes full-size batches run (a few-row batch
+    # would otherwise take mg2d_reg's wide small-batch shapes on levels 7-9)
+    if shapes == "p8":
+        monkeypatch.setenv("HWG_REG_WIDE", "0")
     meta, g = golden("mg10")
     hier = hw.build_mesh_hierarchy(2, 10)
     B = np.random.default_rng(meta["probe_seed"]).standard_normal((meta["rows"], meta["n"]))

@@ -121,8 +121,15 @@ def test_pcg_device_resident_rtol(case):
     assert res.iterations == meta["iterations"]
 
 
+@pytest.mark.parametrize("shapes", ["auto", "p8", "wide"])
 @pytest.mark.parametrize("name", ["mg8", "mg1d10", "mgL8"])
-def test_multigrid_large_K(name):
+def test_multigrid_large_K(name, shapes, monkeypatch):
+    # mg2d_reg thread shapes: the small-batch policy, the default P = 8
+    # shapes of full-size batches, every wide shape
+    if shapes != "auto":
+        if name == "mg1d10":
+            pytest.skip("2D thread shapes")
+        monkeypatch.setenv("HWG_REG_WIDE", "0" if shapes == "p8" else str(0x780))
     meta, g = golden(name)
     hier = hw.build_mesh_hierarchy(meta["d"], meta["K"], meta.get("domain", "square"))
     B = np.random.default_rng(meta["probe_seed"]).standard_normal((meta["rows"], meta["n"]))
@@ -318,7 +325,7 @@ def test_lshape_layout_roundtrip():
 
 
 @pytest.mark.parametrize("domain", ["square", "L"])
-def test_multigrid_K11_matches_oracle(domain):
+def test_multigrid_K11_matches_oracle(domain, monkeypatch):
     """The n = 2047 register kernel (BASELINE cfg 5's finest level K = 11 on
     the mapped L; also the square) against the oracle on seeded rows."""
     from oracle import heatwave_oracle as O
@@ -334,9 +341,17 @@ def test_multigrid_K11_matches_oracle(domain):
     for alpha, mu in ((1.0, 0.0), (0.3, 2.0 ** 11)):
         want = O.Multigrid(ops, prols, alpha, mu).apply_rows(B, np.empty_like(B))
         got = np.empty_like(B)
-        hw.make_solver(hier, alpha, mu, D=D).apply_rows(B, got, 0, 2)
+        solver = hw.make_solver(hier, alpha, mu, D=D)
+        solver.apply_rows(B, got, 0, 2)
+        # the default P = 8 shapes of full-size batches agree with the
+        # small-batch shapes this 2-row batch takes, up to rounding
+        monkeypatch.setenv("HWG_REG_WIDE", "0")
+        got8 = np.empty_like(B)
+        solver.apply_rows(B, got8, 0, 2)
+        monkeypatch.delenv("HWG_REG_WIDE")
         # rounding grows with the level operator's conditioning (~4^K)
         assert relative_diff(got, want) <= 1e-12 * 4.0 ** (K - 8), (alpha, mu)
+        assert relative_diff(got8, want) <= 1e-12 * 4.0 ** (K - 8), (alpha, mu)
 
 
 def test_lshape_cfg5_shaped_properties():
