@@ -56,6 +56,7 @@ struct hwg_ctx {
     hwg_desc d{};
     int dim = 2, J = 0, K = 0, m = 0, nv = 2;
     int mg_reg_ok = 0;                  // every 2D level operator has |beta| <= kRegBetaMax
+    int mg_wide = 0;                    // levels (bit l) mg2d_reg runs with its wide thread shape
     int coarse_fast = 1;                // mg2d_coarse below streamed levels: fast arithmetic
     double *cmat1d = nullptr;           // 1D, K >= 6: [op][15][15] level-4 V-cycle operators
     int mg1d_dense = 1;                 // HWG_MG1D_DENSE=0: the level-4..1 sub-cycle (A/B)
@@ -383,6 +384,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.op = op;
                 a.zero_start = (l < c->K || cyc == 0) ? 1 : 0;
                 a.reg_ok = c->mg_reg_ok;
+                a.wide = c->mg_wide;
                 a.lshape = c->domain;
                 a.diag = level_has_diag(c, l, ro ? -1 : op);
                 const double n2 = (double)level_size(c, l), m2 = (double)level_size(c, l - 1);
@@ -415,6 +417,7 @@ static int mg_apply(hwg_ctx *c, const double *B, double *X, int64_t rows, int op
                 a.row_op = ro;
                 a.op = op;
                 a.reg_ok = c->mg_reg_ok;
+                a.wide = c->mg_wide;
                 a.lshape = c->domain;
                 a.diag = level_has_diag(c, l, ro ? -1 : op);
                 if (fuse && l == c->K && cyc == c->nv - 1) {
@@ -652,6 +655,17 @@ int hwg_create(const hwg_desc *desc, hwg_ctx **out)
     c->scale.assign(d.wavelet_scale, d.wavelet_scale + d.J);
     const int nops = d.J + 2;
     c->coef_host.assign(d.coef, d.coef + (size_t)nops * (d.K + 1) * HWG_COEF_STRIDE);
+    // mg2d_reg thread shapes are a property of the context (the global time
+    // axis), never of a call's batch: results do not depend on how rows are
+    // batched or split over time slabs.  Few temporal rows leave each SM one
+    // or two warps of a level <= 9 pass; the wide shapes halve a thread's
+    // points (hw_mg2d_reg.cu, profiles/r02/mg_wide_sweep.txt)
+    {
+        const int64_t n_t = ((int64_t)1 << d.J) + 1;
+        if (n_t <= kWideWarps) c->mg_wide |= (1 << 7) | (1 << 8);
+        if (2 * n_t <= kWideWarps) c->mg_wide |= 1 << 9;
+        if (d.domain && n_t <= 148) c->mg_wide |= 1 << 10;
+    }
     c->mg_reg_ok = 1;
     for (int op = 0; op < nops; ++op)
         for (int l = 1; l <= d.K; ++l) {

@@ -21,6 +21,7 @@ struct MgStreamArgs {
     int op;                             // default operator
     int zero_start;                     // DOWN: iterate starts at zero
     int reg_ok;                         // |beta| small enough for mg2d_reg
+    int wide;                           // mg2d_reg: levels (bit l) run with the wide thread shape
     const double *dot_y;                // UP (mg2d_reg): dot_part[row] = <dot_y row, final X row>
     double *dot_part;
     int lshape;                         // mapped L-shaped domain (mg2d_reg only)
@@ -50,8 +51,8 @@ cudaError_t mg2d_stream_launch(const MgStreamArgs &a, bool down, int64_t rows, c
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st);
 // largest |beta| = |cy / c0| mg2d_reg accepts (8-chunk window: |beta|^32 <= 2^-60)
 constexpr double kRegBetaMax = 0.2726;
-// mg2d_reg_launch: levels 7-9 switch to twice the threads per row while the
-// batch has at most kWideWarps default-shape warps (~2 per SM)
+// mg2d_reg: levels 7-9 run with twice the threads per row in contexts whose
+// N_t-row batches have at most kWideWarps default-shape warps (~2 per SM)
 constexpr int64_t kWideWarps = 320;
 cudaError_t mg2d_coarse_launch(const MgCoarseArgs &a, cudaStream_t st);
 

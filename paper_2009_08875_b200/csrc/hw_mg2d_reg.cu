@@ -774,29 +774,27 @@ cudaError_t launch_reg_n(const MgStreamArgs &a, bool down, int64_t rows, cudaStr
 }  // namespace
 
 // Thread shape per level.  The default shapes (P = 8 points per thread) are
-// the HBM-efficient ones for batches of a wave or more.  A small batch leaves
-// each SM with one or two warps of a level <= 9 pass, each issuing a whole
-// grid row's three sweeps alone (issue- and latency-bound); the WIDE shapes
-// split the row over 2x the threads (P = 4 / 2, the same 32-column carry
-// window, results equal up to rounding).  Measured (scripts/mg_wide_sweep.py,
-// profiles/r02/mg_wide_sweep.txt): a gain while rows x default warps per row
-// <= ~2 per SM (K = 8: -15 % at 129 rows, -11 % at 257; K = 10: -6 % at 136
-// rows), a loss above; level 10 only for the L-shaped variant at <= 1 row per
-// SM (its P = 8 DOWN pass spills).  HWG_REG_WIDE=<bitmask of levels> forces
-// a choice (A/B and the parity tests of the default shapes), 0 = never.
-static int wide_mask(const MgStreamArgs &a, int64_t rows)
+// the HBM-efficient ones for batches of a wave or more.  A short time axis
+// leaves each SM with one or two warps of a level <= 9 pass, each issuing a
+// whole grid row's three sweeps alone (issue- and latency-bound); the WIDE
+// shapes split the row over 2x the threads (P = 4 / 2, the same 32-column
+// carry window, results equal up to rounding).  Measured
+// (scripts/mg_wide_sweep.py, profiles/r02/mg_wide_sweep.txt): a gain while
+// rows x default warps per row <= ~2 per SM (K = 8: -15 % at 129 rows, -11 %
+// at 257; K = 10: -6 % at 136 rows), a loss above; level 10 only for the
+// L-shaped variant at <= 1 row per SM (its P = 8 DOWN pass spills).  The
+// choice (a.wide) is made once per context from N_t by hwg_create, so results
+// never depend on a call's batch size.  HWG_REG_WIDE=<bitmask of levels>
+// overrides it per launch (A/B and the parity tests of both shapes).
+static int wide_mask(const MgStreamArgs &a)
 {
-    if (const char *ev = getenv("HWG_REG_WIDE")) return atoi(ev);   // read per launch
-    int m = 0;
-    if (rows <= kWideWarps) m |= (1 << 7) | (1 << 8);                // one warp per row
-    if (2 * rows <= kWideWarps) m |= 1 << 9;                         // two warps per row
-    if (a.lshape && rows <= 148) m |= 1 << 10;
-    return m;
+    if (const char *ev = getenv("HWG_REG_WIDE")) return atoi(ev);
+    return a.wide;
 }
 
 cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
-    const int wide = wide_mask(a, rows);
+    const int wide = wide_mask(a);
     switch (a.n) {
     case 63: return launch_reg_n<2, 32, 1>(a, down, rows, st);
     case 127:
