@@ -86,6 +86,26 @@ HW_DEV void cp_async8s(unsigned saddr, const void *gmem, bool skip)
 
 constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 
+// ---- thread-block cluster helpers (CL = 2 column strips of one temporal row) ----
+HW_DEV unsigned cluster_ctarank()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+HW_DEV void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// store v at the address `local` has in CTA `rank` of the cluster (DSMEM)
+HW_DEV void st_cluster(double *local, unsigned rank, double v)
+{
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(r), "d"(v) : "memory");
+}
+
 // shared-memory words (doubles) of one CTA.  Fine rows are staged whole
 // (cooperative, coalesced copies) in slots of RS words with a 16-byte-unit
 // XOR swizzle, so a thread's own chunk reads are conflict-free LDS.128.
@@ -101,7 +121,7 @@ struct RegSmem {
     static constexpr int X0 = (DOWN && ZS) ? 0 : NX * RS;   // x0 ring
     static constexpr int C = DOWN ? 0 : NCR * CS;           // coarse ring (UP)
     static constexpr int O = RS;                            // output row
-    static constexpr int H = 7 * (NW + 1);                  // halos, carries
+    static constexpr int H = 8 * (NW + 1);                  // halos, carries, cluster dot share
     static constexpr int total = B + X0 + C + O + H;
 };
 
@@ -109,10 +129,19 @@ struct RegSmem {
 // row i has parity L0 ^ (i & 1) because a grid row is n (odd) words long
 // DG: the operator has diagonal couplings (c_d != 0, every C_j = alpha A +
 // mu M); DG = false (K_x = A_x, a 5-point stencil) drops them at compile time
-template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0, bool LSH, bool DG>
+// CL = 2: the grid row is split into two column strips of P NT columns, one
+// per CTA of a thread-block cluster (n + 1 = 2 P NT; BASELINE cfg 5's n =
+// 2047 with the footprint of the n = 1023 kernel, so two CTAs of different
+// temporal rows share an SM instead of one phase-locked 256-thread CTA).
+// The truncated carry into the right strip is the left strip's last-warp
+// windowed total; the left strip's right halos are the right strip's first
+// new values: six doubles per step cross the pair through distributed shared
+// memory, ordered by the two per-step barriers (cluster-wide instead of
+// CTA-wide).  Same chunks, windows and arithmetic as one CTA of 2 NT threads.
+template <int P, int NT, bool DOWN, bool ZS, int LB0, int LX0, bool LSH, bool DG, int CL = 1>
 struct RegPass {
     static constexpr int NW = NT / 32;
-    static constexpr int n = P * NT - 1;
+    static constexpr int n = CL * P * NT - 1;
     static constexpr int m = (n - 1) / 2;
     static constexpr int WIN = 32 / P;                 // chunk ends in the carry window
     static constexpr int LEV = ilog2c(WIN);            // shuffle-scan levels
@@ -122,11 +151,14 @@ struct RegPass {
     using SM = RegSmem<P, NT, DOWN, ZS>;
     static constexpr int RS = SM::RS, CS = SM::CS;
     static_assert(P % 2 == 0 && 32 % P == 0 && P >= 2 && CS >= (P / 2) * (NT - 1) + NC &&
-                      CS >= m + 2, "chunk layout");
+                      CS >= (CL == 1 ? m + 2 : (P / 2) * NT + 4) && (CL == 1 || CL == 2),
+                  "chunk layout");
     static constexpr int gs = DOWN ? 1 : -1;           // UP runs point-reversed
 
     // ---- per-CTA / per-thread constants ----
     int tid, lane, warp;
+    int crank, col0, gt;                  // cluster rank, first column of the strip, chunk number in the row
+    bool lstrip;                          // the strip that ends with column n
     bool last;                            // owns column n (a zero pad)
     double cxs, cds, c0, inv, beta;       // cx/c0, cd/c0, c0, 1/c0, -cy/c0
     double bp[P];                         // beta^(k+1)
@@ -178,8 +210,12 @@ struct RegPass {
         tid = threadIdx.x;
         lane = tid & 31;
         warp = tid >> 5;
-        last = tid == NT - 1;
-        const int64_t row = blockIdx.x;
+        crank = CL > 1 ? (int)cluster_ctarank() : 0;
+        col0 = crank * P * NT;
+        gt = crank * NT + tid;
+        lstrip = crank == CL - 1;
+        last = lstrip && tid == NT - 1;
+        const int64_t row = blockIdx.x / CL;
         const int op = a.row_op ? a.row_op[row] : a.op;
         const double *cf = a.coef + ((int64_t)op * a.levels_p1 + a.level) * kCoefStride;
         inv = cf[kInv];
@@ -200,7 +236,7 @@ struct RegPass {
         Bg = a.B + row * a.ldB;
         Xg = a.X + row * a.ldX;
         Xcg = DOWN ? nullptr : a.Xc + row * a.ldXc;
-        Bcg = DOWN ? a.Bc + row * a.ldBc + (P / 2) * tid : nullptr;
+        Bcg = DOWN ? a.Bc + row * a.ldBc + (P / 2) * gt : nullptr;
         Dg = (!DOWN && a.dot_y) ? a.dot_y + row * a.ldX : nullptr;
         dsum = 0.0;
         bsm = sm;
@@ -217,7 +253,7 @@ struct RegPass {
         if constexpr (LSH) {
 #pragma unroll
             for (int k = 0; k < P; ++k)
-                if (DOWN ? (P * tid + k >= m) : (P * tid + k <= m)) cm |= 1u << k;
+                if (DOWN ? (P * gt + k >= m) : (P * gt + k <= m)) cm |= 1u << k;
         }
 #pragma unroll
         for (int h = 0; h <= P / 2; ++h) ooff[h] = phys(P * tid + 2 * h);
@@ -241,10 +277,10 @@ struct RegPass {
         for (int q = 0; q < NC; ++q) HC[q] = 0.0;          // coarse row -1
     }
 
-    // global element of (grid row i, local column j); UP is point-reversed
-    static HW_DEV int64_t gidx(int i, int j)
+    // global element of (grid row i, strip column j); UP is point-reversed
+    HW_DEV int64_t gidx(int i, int j) const
     {
-        return DOWN ? (int64_t)i * n + j : (int64_t)(n - 1 - i) * n + (n - 1 - j);
+        return DOWN ? (int64_t)i * n + (col0 + j) : (int64_t)(n - 1 - i) * n + (n - 1 - col0 - j);
     }
 
     HW_DEV int koff(int k) const { return LIN ? k * NT : phys(tid + k * NT) - cpo; }
@@ -269,29 +305,37 @@ struct RegPass {
             if constexpr (ZERO) {
 #pragma unroll
                 for (int k = 0; k < P; ++k) slot[tid + k * NT] = 0.0;
+                if (CL > 1 && !lstrip && tid == 0) slot[phys(P * NT)] = slot[phys(P * NT) + 1] = 0.0;
             }
             return;
         }
-        const double *row0 = src + gidx(i, 0);               // local column 0
+        const double *row0 = src + gidx(i, 0);               // strip column 0
+        // CL > 1: a strip that is not the last also stages the unit after it
+        // (the next strip's first columns: the last thread's right halo)
+        const bool xhalo = CL > 1 && !lstrip && tid == 0;
+        const unsigned xs = smem_u32(slot + phys(P * NT));
         if constexpr (DOWN) {
             if ((reinterpret_cast<uintptr_t>(row0) & 15) == 0) {
                 const unsigned sa = smem_u32(slot + phys(2 * tid));
 #pragma unroll
                 for (int k = 0; k < P / 2; ++k) {
                     const int q = tid + k * NT;              // pair (2q, 2q+1)
-                    const bool skip = LSH && i >= m && 2 * q >= m;   // removed quadrant
-                    if (k < P / 2 - 1 || tid < NT - 1)
+                    const bool skip = LSH && i >= m && col0 + 2 * q >= m;   // removed quadrant
+                    if (k < P / 2 - 1 || tid < NT - 1 || !lstrip)
                         cp_async16s(sa + 16u * k * NT, row0 + 2 * q, skip);
                     else                                     // column n-1 only (n is a pad)
                         cp_async8s(sa + 16u * k * NT, row0 + 2 * q, skip);
                 }
+                if (xhalo) cp_async16s(xs, row0 + P * NT, LSH && i >= m && col0 + P * NT >= m);
             } else {
                 const double *g = row0 + tid;
                 const unsigned sa = smem_u32(slot + cpo);
 #pragma unroll
                 for (int k = 0; k < P; ++k)
-                    if (k < P - 1 || tid < NT - 1)
-                        cp_async8s(sa + 8u * koff(k), g + k * NT, LSH && i >= m && tid + k * NT >= m);
+                    if (k < P - 1 || tid < NT - 1 || !lstrip)
+                        cp_async8s(sa + 8u * koff(k), g + k * NT,
+                                   LSH && i >= m && col0 + tid + k * NT >= m);
+                if (xhalo) cp_async8s(xs, row0 + P * NT, LSH && i >= m && col0 + P * NT >= m);
             }
         } else {
             const unsigned sa = smem_u32(slot + phys(2 * tid));
@@ -300,8 +344,8 @@ struct RegPass {
                 const int q = tid + k * NT;                  // unit q
                 const unsigned d = sa + 16u * k * NT;
                 if constexpr (LR == 0) {                     // columns (2q, 2q+1)
-                    if (k < P / 2 - 1 || tid < NT - 1) {
-                        cp_async16s(d, row0 - 2 * q - 1, LSH && i <= m && 2 * q + 1 <= m);
+                    if (k < P / 2 - 1 || tid < NT - 1 || !lstrip) {
+                        cp_async16s(d, row0 - 2 * q - 1, LSH && i <= m && col0 + 2 * q + 1 <= m);
                     } else {                                 // (n-1, n): column n-1 only;
                         cp_async8s(d + 8u, row0 - 2 * q);
                         // the pad n: the slot may last have held a parity-1
@@ -309,9 +353,16 @@ struct RegPass {
                         slot[phys(2 * q)] = 0.0;
                     }
                 } else {                                     // columns (2q-1, 2q)
-                    if (k > 0 || tid > 0) cp_async16s(d, row0 - 2 * q, LSH && i <= m && 2 * q <= m);
+                    if (k > 0 || tid > 0 || crank > 0)
+                        cp_async16s(d, row0 - 2 * q, LSH && i <= m && col0 + 2 * q <= m);
                     else cp_async8s(d, row0);                // (-1, 0): column 0 only
                 }
+            }
+            if (xhalo) {
+                if constexpr (LR == 0)                       // columns (P NT, P NT + 1)
+                    cp_async16s(xs, row0 - P * NT - 1, LSH && i <= m && col0 + P * NT + 1 <= m);
+                else                                         // columns (P NT - 1, P NT)
+                    cp_async16s(xs, row0 - P * NT, LSH && i <= m && col0 + P * NT <= m);
             }
         }
     }
@@ -320,6 +371,22 @@ struct RegPass {
     HW_DEV void stage_coarse(int ic, int slotno) const
     {
         if (ic > m) return;
+        if constexpr (CL > 1) {
+            // strip: slot index x holds coarse column (P/2) NT crank + x - 1;
+            // indices whose column does not exist are never written (zero)
+            double *slot = csm + (size_t)slotno * CS;
+            constexpr int mc = (m - 1) / 2;
+            for (int x = tid; x < (P / 2) * NT + 4; x += NT) {
+                const int J = (P / 2) * NT * crank + x - 1;
+                if (J < 0 || J >= m) continue;
+                double *d = slot + cphys(x);
+                if (ic < 0 || ic == m) *d = 0.0;
+                else
+                    cp_async8s(smem_u32(d), Xcg + (int64_t)(m - 1 - ic) * m + (m - 1 - J),
+                               LSH && ic <= mc && J <= mc);
+            }
+            return;
+        }
         static_assert((NT / 16) % 2 == 0, "coarse swizzle periodic in NT");
         double *slot = csm + (size_t)slotno * CS + cphys(1 + tid);
         if (ic < 0 || ic == m) {
@@ -437,12 +504,12 @@ struct RegPass {
         for (int k = 0; k < P; ++k) v[k] = osm[cpo + koff(k)];
 #pragma unroll
         for (int k = 0; k < P; ++k)
-            if (k < P - 1 || tid < NT - 1) g[gs * k * NT] = v[k];
+            if (k < P - 1 || tid < NT - 1 || !lstrip) g[gs * k * NT] = v[k];
         if (!DOWN && Dg) {                       // fused inner product, fixed order
             const double *d = Dg + gidx(i, 0) + gs * tid;
 #pragma unroll
             for (int k = 0; k < P; ++k)
-                if (k < P - 1 || tid < NT - 1) dsum = fma(d[gs * k * NT], v[k], dsum);
+                if (k < P - 1 || tid < NT - 1 || !lstrip) dsum = fma(d[gs * k * NT], v[k], dsum);
         }
     }
 
@@ -461,7 +528,18 @@ struct RegPass {
             double u = lane < NW ? tot[lane] : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
-            if (lane == 0) a.dot_part[blockIdx.x] = u;
+            if constexpr (CL == 1) {
+                if (lane == 0) a.dot_part[blockIdx.x] = u;
+            } else {
+                double *xdot = tot + 3 * HS;               // [2], used only here
+                if (lane == 0 && crank > 0) st_cluster(&xdot[1], 0, u);   // the right strip's share
+                if (lane == 0) xdot[0] = u;
+            }
+        }
+        if constexpr (CL > 1) {
+            cluster_sync_all();
+            const double *xdot = tot + 3 * HS;
+            if (crank == 0 && tid == 0) a.dot_part[blockIdx.x / CL] = xdot[0] + xdot[1];
         }
     }
 
@@ -532,7 +610,7 @@ struct RegPass {
         const bool vo = !EDGE || (t >= 5 && t - 5 < n);
 
         cp_async_wait<2>();                              // own copies of step t-3 landed
-        __syncthreads();                                 // (A) all copies, halos, output row visible
+        sync_pair();                                     // (A) all copies, halos, output row visible
         if (vo) flush(t - 5);                            // row t-5, staged last step
         if (lane == 31) {
             X1R[Q] = HR[0 * HS + warp + 1];
@@ -576,6 +654,7 @@ struct RegPass {
                     if ((rr >> k) & 1u) R[k] = 0.0;
             }
             if (lane == 0) HRes[warp] = R[0];
+            if (CL > 1 && crank > 0 && tid == 0) st_cluster(&HRes[NW], crank - 1, R[0]);
         }
 
         double A[3];
@@ -584,8 +663,12 @@ struct RegPass {
         if (lane == 31) {
 #pragma unroll
             for (int s = 0; s < 3; ++s) tot[s * HS + warp + 1] = A[s];
+            if (CL > 1 && !lstrip && warp == NW - 1) {   // the carry window into the next strip
+#pragma unroll
+                for (int s = 0; s < 3; ++s) st_cluster(&tot[s * HS], crank + 1, A[s]);
+            }
         }
-        __syncthreads();                                 // (B) warp totals visible, output row
+        sync_pair();                                     // (B) warp totals visible, output row
                                                          //     and the oldest ring slots free
         issue<PAR>(t);
 
@@ -634,6 +717,11 @@ struct RegPass {
             HR[0 * HS + warp] = xn[0][0];
             HR[1 * HS + warp] = xn[1][0];
             if constexpr (DOWN) HR[2 * HS + warp] = dl[0];
+            if (CL > 1 && crank > 0 && warp == 0) {      // the previous strip's right halos
+                st_cluster(&HR[0 * HS + NW], crank - 1, xn[0][0]);
+                st_cluster(&HR[1 * HS + NW], crank - 1, xn[1][0]);
+                if constexpr (DOWN) st_cluster(&HR[2 * HS + NW], crank - 1, dl[0]);
+            }
         }
         if constexpr (!(DOWN && ZS)) {
 #pragma unroll
@@ -665,6 +753,13 @@ struct RegPass {
         if (PAR) sc = sc + 1 == SM::NCR ? 0 : sc + 1;
     }
 
+    // the step barriers: CTA-wide, or cluster-wide when the row is split
+    HW_DEV void sync_pair() const
+    {
+        if constexpr (CL > 1) cluster_sync_all();
+        else __syncthreads();
+    }
+
     HW_DEV void advance()
     {
         sb = sb + 1 == SM::NB ? 0 : sb + 1;
@@ -675,7 +770,8 @@ struct RegPass {
     {
         // prologue: x0 row 0 (+ coarse rows -1, 0), then the groups steps
         // -3..-1 would have issued
-        __syncthreads();                                 // zeroed slots before any copy lands
+        sync_pair();                                     // zeroed slots before any copy lands
+                                                         // (or any store of the other strip)
         if constexpr (!(DOWN && ZS)) {
             stage_row<true, LX0>(x0sm, Xg, 0);
             if constexpr (!DOWN) {
@@ -716,59 +812,77 @@ struct RegPass {
     }
 };
 
-template <int P, int NT, bool DOWN, bool ZS, int LB, int LX, bool LSH, bool DG>
+template <int P, int NT, bool DOWN, bool ZS, int LB, int LX, bool LSH, bool DG, int CL>
 HW_DEV void run_pass(const MgStreamArgs &a, double *sm)
 {
-    RegPass<P, NT, DOWN, ZS, LB, LX, LSH, DG> p(a, sm);
+    RegPass<P, NT, DOWN, ZS, LB, LX, LSH, DG, CL> p(a, sm);
     p.run();
     p.finish_dot(a);
+    if constexpr (CL > 1) cluster_sync_all();            // no strip exits under the other's stores
 }
 
-template <int P, int NT, bool DOWN, bool ZS, int MINB, bool LSH, bool DG>
+template <int P, int NT, bool DOWN, bool ZS, int MINB, bool LSH, bool DG, int CL>
 __global__ void __launch_bounds__(NT, MINB) mg2d_reg(MgStreamArgs a)
 {
     extern __shared__ __align__(16) double sm[];
     if constexpr (DOWN) {
-        run_pass<P, NT, DOWN, ZS, 0, 0, LSH, DG>(a, sm);
+        run_pass<P, NT, DOWN, ZS, 0, 0, LSH, DG, CL>(a, sm);
     } else {
         // UP: layout parity of grid row 0 (stage_row) = 1 when local column 0
-        // (global row n-1, column n-1) sits at a 16-byte boundary
-        constexpr int n = P * NT - 1;
-        const int64_t row = blockIdx.x;
+        // (global row n-1, column n-1) sits at a 16-byte boundary (the strips
+        // of a split row start an even number of columns apart: same parity)
+        constexpr int n = CL * P * NT - 1;
+        const int64_t row = blockIdx.x / CL;
         auto parity = [&](const double *base, int64_t ld) -> int {
             const double *p0 = base + row * ld + (int64_t)(n - 1) * n + (n - 1);
             return 1 - (int)((reinterpret_cast<uintptr_t>(p0) >> 3) & 1);
         };
         const int lb = parity(a.B, a.ldB), lx = parity(a.X, a.ldX);
         if (lb) {
-            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1, LSH, DG>(a, sm);
-            else run_pass<P, NT, DOWN, ZS, 1, 0, LSH, DG>(a, sm);
+            if (lx) run_pass<P, NT, DOWN, ZS, 1, 1, LSH, DG, CL>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 1, 0, LSH, DG, CL>(a, sm);
         } else {
-            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1, LSH, DG>(a, sm);
-            else run_pass<P, NT, DOWN, ZS, 0, 0, LSH, DG>(a, sm);
+            if (lx) run_pass<P, NT, DOWN, ZS, 0, 1, LSH, DG, CL>(a, sm);
+            else run_pass<P, NT, DOWN, ZS, 0, 0, LSH, DG, CL>(a, sm);
         }
     }
 }
 
-template <int P, int NT, bool DOWN, bool ZS, int MINB>
+template <int P, int NT, bool DOWN, bool ZS, int MINB, int CL>
 cudaError_t launch_reg_t(const MgStreamArgs &a, int64_t rows, cudaStream_t st)
 {
     const size_t smem = RegSmem<P, NT, DOWN, ZS>::total * sizeof(double);
-    auto k = a.lshape ? mg2d_reg<P, NT, DOWN, ZS, MINB, true, true>
-                      : (a.diag ? mg2d_reg<P, NT, DOWN, ZS, MINB, false, true>
-                                : mg2d_reg<P, NT, DOWN, ZS, MINB, false, false>);
+    auto k = a.lshape ? mg2d_reg<P, NT, DOWN, ZS, MINB, true, true, CL>
+                      : (a.diag ? mg2d_reg<P, NT, DOWN, ZS, MINB, false, true, CL>
+                                : mg2d_reg<P, NT, DOWN, ZS, MINB, false, false, CL>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<(unsigned)rows, NT, smem, st>>>(a);
-    return cudaGetLastError();
+    if constexpr (CL == 1) {
+        k<<<(unsigned)rows, NT, smem, st>>>(a);
+        return cudaGetLastError();
+    } else {                                             // one cluster of CL strips per temporal row
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(rows * CL), 1, 1);
+        cfg.blockDim = dim3(NT, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k, a);
+    }
 }
 
-template <int P, int NT, int MINB>
+template <int P, int NT, int MINB, int CL = 1>
 cudaError_t launch_reg_n(const MgStreamArgs &a, bool down, int64_t rows, cudaStream_t st)
 {
-    if (!down) return launch_reg_t<P, NT, false, false, MINB>(a, rows, st);
-    return a.zero_start ? launch_reg_t<P, NT, true, true, MINB>(a, rows, st)
-                        : launch_reg_t<P, NT, true, false, MINB>(a, rows, st);
+    if (!down) return launch_reg_t<P, NT, false, false, MINB, CL>(a, rows, st);
+    return a.zero_start ? launch_reg_t<P, NT, true, true, MINB, CL>(a, rows, st)
+                        : launch_reg_t<P, NT, true, false, MINB, CL>(a, rows, st);
 }
 
 }  // namespace
@@ -813,8 +927,11 @@ cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cuda
             return launch_reg_n<4, 256, 1>(a, down, rows, st);
         return launch_reg_n<8, 128, 2>(a, down, rows, st);
     case 2047:
-        if (wide & (1 << 11)) return launch_reg_n<4, 512, 1>(a, down, rows, st);
-        return launch_reg_n<8, 256, 1>(a, down, rows, st);
+        // two 128-thread strips per row on a CTA pair (two rows per SM);
+        // HWG_REG_CLUSTER=0: one 256-thread CTA per row (A/B)
+        if (const char *ev = getenv("HWG_REG_CLUSTER"))
+            if (ev[0] == '0') return launch_reg_n<8, 256, 1>(a, down, rows, st);
+        return launch_reg_n<8, 128, 2, 2>(a, down, rows, st);
     default: return cudaErrorNotSupported;
     }
 }

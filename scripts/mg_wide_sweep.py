@@ -20,7 +20,13 @@ ap.add_argument("--rows", type=int, nargs="+", default=[64, 136, 148, 272, 296, 
 ap.add_argument("--masks", type=int, nargs="+", default=[0, 128, 384, 896])
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--domain", default="square")
+ap.add_argument("--var", default="HWG_REG_WIDE", help="env variable the values are tried on "
+                "(HWG_REG_CLUSTER: 0 = one 256-thread CTA per n = 2047 row, 1 = CTA pair)")
+ap.add_argument("--fixed", nargs="*", default=[], help="NAME=VALUE settings held fixed")
 a = ap.parse_args()
+for kv in a.fixed:
+    name, val = kv.split("=")
+    os.environ[name] = val
 rmax = max(a.rows)
 kw = {"domain": "L"} if a.domain == "L" else {}
 ctx = GpuContext(2, 3, a.K, rows_max=rmax, **kw)
@@ -32,7 +38,7 @@ ref = None
 for R in a.rows:
     line = [f"rows {R:5d}"]
     for mask in a.masks:
-        os.environ["HWG_REG_WIDE"] = str(mask)
+        os.environ[a.var] = str(mask)
         ctx.mg_rows_dev(ops[:R], B[:R], X[:R])
         torch.cuda.synchronize()
         if mask == a.masks[0]:
@@ -40,6 +46,8 @@ for R in a.rows:
         else:
             d = float((X[:4] - ref).abs().max() / ref.abs().max())
             assert d < 1e-11, (mask, d)
+            if d != 0.0:
+                line.append(f"[diff {d:.1e}]")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(a.reps):
