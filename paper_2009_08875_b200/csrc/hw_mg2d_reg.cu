@@ -98,12 +98,52 @@ HW_DEV void cluster_sync_all()
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+HW_DEV unsigned mapa_u32(unsigned saddr, unsigned rank)
+{
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
 // store v at the address `local` has in CTA `rank` of the cluster (DSMEM)
 HW_DEV void st_cluster(double *local, unsigned rank, double v)
 {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
-    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(r), "d"(v) : "memory");
+    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(mapa_u32(smem_u32(local), rank)), "d"(v)
+                 : "memory");
+}
+// Per-step messages between the strips: the sender's st.async writes a
+// double into the receiver's mailbox and completes 8 bytes of the receiver's
+// mbarrier transaction count (STAS: no fence, no L1 invalidation -- a
+// st.release.cluster costs MEMBAR.ALL.GPU, a barrier.cluster ~1.7k cycles
+// here); the receiver arms the phase with arrive.expect_tx and polls
+// try_wait.parity.
+HW_DEV void mbar_init(unsigned mb, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mb), "r"(count) : "memory");
+}
+HW_DEV void mbar_expect(unsigned mb, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bytes)
+                 : "memory");
+}
+HW_DEV void mbar_wait(unsigned mb, unsigned parity)
+{
+    unsigned done = 0;
+    int spins = 0;
+    while (!done) {
+        asm volatile("{\n.reg .pred p;\n"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     "selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(mb), "r"(parity)
+                     : "memory");
+        if (!done && ++spins > (1 << 22)) __trap();      // never hang the GPU on a lost message
+    }
+}
+HW_DEV void st_async_f64(unsigned raddr, double v, unsigned rmbar)
+{
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(raddr),
+                 "d"(v), "r"(rmbar)
+                 : "memory");
 }
 
 // shared-memory words (doubles) of one CTA.  Fine rows are staged whole
@@ -121,7 +161,8 @@ struct RegSmem {
     static constexpr int X0 = (DOWN && ZS) ? 0 : NX * RS;   // x0 ring
     static constexpr int C = DOWN ? 0 : NCR * CS;           // coarse ring (UP)
     static constexpr int O = RS;                            // output row
-    static constexpr int H = 8 * (NW + 1);                  // halos, carries, cluster dot share
+    static constexpr int H = 8 * (NW + 1) + 20;             // halos, carries, cluster dot share,
+                                                            // strip mailboxes + mbarriers
     static constexpr int total = B + X0 + C + O + H;
 };
 
@@ -170,6 +211,8 @@ struct RegPass {
     double dsum;                          //     this thread's share of <Dg, X>
     double *bsm, *x0sm, *csm, *osm;
     double *HR, *HRes, *tot;              // [3][HS], [1][HS], [3][HS]
+    double *box_tot, *box_hr, *box_res;   // CL > 1 mailboxes [2][3], [2][3], [2] (slot = step parity)
+    unsigned mb_tot, mb_hr, mb_res;       //         their mbarriers (shared addresses)
     int cpo;                              // slot position of column tid (copy / flush lane)
     int hoff;                             // DOWN: slot position of the right-halo column P (t+1)
     int ooff[P / 2 + 1];                  // slot positions of units P t/2 .. P t/2 + P/2
@@ -246,6 +289,12 @@ struct RegPass {
         HR = osm + SM::O;
         HRes = HR + 3 * HS;
         tot = HRes + HS;
+        box_tot = tot + 3 * HS + 2;                        // (+2: the cluster dot share)
+        box_hr = box_tot + 6;
+        box_res = box_hr + 6;
+        mb_tot = smem_u32(box_res + 2);
+        mb_hr = mb_tot + 8;
+        mb_res = mb_hr + 8;
         for (int k = tid; k < SM::total; k += NT) sm[k] = 0.0;   // pads stay zero
         cpo = phys(tid);
         hoff = phys(P * (tid + 1));
@@ -610,12 +659,23 @@ struct RegPass {
         const bool vo = !EDGE || (t >= 5 && t - 5 < n);
 
         cp_async_wait<2>();                              // own copies of step t-3 landed
-        sync_pair();                                     // (A) all copies, halos, output row visible
+        __syncthreads();                                 // (A) all copies, halos, output row visible
         if (vo) flush(t - 5);                            // row t-5, staged last step
         if (lane == 31) {
             X1R[Q] = HR[0 * HS + warp + 1];
             X2R[Q] = HR[1 * HS + warp + 1];
             if constexpr (DOWN) DR[Q] = HR[2 * HS + warp + 1];
+        }
+        if constexpr (CL > 1) {
+            if (crank > 0 && tid == 0) mbar_expect(mb_tot, 24);          // this step's carry windows
+            if (!lstrip && warp == NW - 1 && lane == 31) {
+                if (t > 0) mbar_wait(mb_hr, Q);                          // the next strip's halos of step t-1
+                X1R[Q] = box_hr[Q * 3 + 0];
+                X2R[Q] = box_hr[Q * 3 + 1];
+                if constexpr (DOWN) DR[Q] = box_hr[Q * 3 + 2];
+                mbar_expect(mb_hr, DOWN ? 24 : 16);                      // ... and of this step
+                if constexpr (DOWN) mbar_expect(mb_res, 8);
+            }
         }
 
         // ---- phase A: chunk recurrences of the three sweeps ----
@@ -654,7 +714,8 @@ struct RegPass {
                     if ((rr >> k) & 1u) R[k] = 0.0;
             }
             if (lane == 0) HRes[warp] = R[0];
-            if (CL > 1 && crank > 0 && tid == 0) st_cluster(&HRes[NW], crank - 1, R[0]);
+            if (CL > 1 && crank > 0 && tid == 0)
+                st_async_f64(mapa_u32(smem_u32(box_res + PAR), crank - 1), R[0], mapa_u32(mb_res, crank - 1));
         }
 
         double A[3];
@@ -664,20 +725,25 @@ struct RegPass {
 #pragma unroll
             for (int s = 0; s < 3; ++s) tot[s * HS + warp + 1] = A[s];
             if (CL > 1 && !lstrip && warp == NW - 1) {   // the carry window into the next strip
+                const unsigned rb = mapa_u32(smem_u32(box_tot + PAR * 3), crank + 1);
+                const unsigned rm = mapa_u32(mb_tot, crank + 1);
 #pragma unroll
-                for (int s = 0; s < 3; ++s) st_cluster(&tot[s * HS], crank + 1, A[s]);
+                for (int s = 0; s < 3; ++s) st_async_f64(rb + 8u * s, A[s], rm);
             }
         }
-        sync_pair();                                     // (B) warp totals visible, output row
+        __syncthreads();                                 // (B) warp totals visible, output row
                                                          //     and the oldest ring slots free
         issue<PAR>(t);
 
         // ---- phase B: carries, new rows, halos ----
         double xn[3][P], cin[3];
+        const bool inbox = CL > 1 && crank > 0 && warp == 0;    // the previous strip's windows
+        if (inbox) mbar_wait(mb_tot, PAR);
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
             const double prev = __shfl_up_sync(0xffffffffu, A[s], 1);
-            cin[s] = fma(gl, tot[s * HS + warp], lane ? prev : 0.0);
+            const double tprev = inbox ? box_tot[PAR * 3 + s] : tot[s * HS + warp];
+            cin[s] = fma(gl, tprev, lane ? prev : 0.0);
             const bool vs = s == 0 ? v1 : (s == 1 ? v2 : v3);
             const unsigned rms = s == 0 ? rm0 : (s == 1 ? rm1 : rm2);
 #pragma unroll
@@ -718,9 +784,11 @@ struct RegPass {
             HR[1 * HS + warp] = xn[1][0];
             if constexpr (DOWN) HR[2 * HS + warp] = dl[0];
             if (CL > 1 && crank > 0 && warp == 0) {      // the previous strip's right halos
-                st_cluster(&HR[0 * HS + NW], crank - 1, xn[0][0]);
-                st_cluster(&HR[1 * HS + NW], crank - 1, xn[1][0]);
-                if constexpr (DOWN) st_cluster(&HR[2 * HS + NW], crank - 1, dl[0]);
+                const unsigned rb = mapa_u32(smem_u32(box_hr + PAR * 3), crank - 1);
+                const unsigned rm = mapa_u32(mb_hr, crank - 1);
+                st_async_f64(rb, xn[0][0], rm);
+                st_async_f64(rb + 8u, xn[1][0], rm);
+                if constexpr (DOWN) st_async_f64(rb + 16u, dl[0], rm);
             }
         }
         if constexpr (!(DOWN && ZS)) {
@@ -731,9 +799,15 @@ struct RegPass {
         // ---- restriction of residual row r = t-6 (parity PAR) ----
         // coarse column J = (P/2) t + q collects fine columns 2J, 2J+1, 2J+2
         if constexpr (DOWN) {
+            double rbox = 0.0;                           // CL > 1: consumed every step (phases stay in step)
+            const bool rin = CL > 1 && !lstrip && warp == NW - 1 && lane == 31;
+            if (rin) {
+                mbar_wait(mb_res, PAR);
+                rbox = box_res[PAR];
+            }
             if (vr) {
                 double RR = __shfl_down_sync(0xffffffffu, R[0], 1);
-                if (lane == 31) RR = HRes[warp + 1];
+                if (lane == 31) RR = rin ? rbox : HRes[warp + 1];
                 const int r = t - 6;
 #pragma unroll
                 for (int q = 0; q < P / 2; ++q) {
@@ -770,8 +844,17 @@ struct RegPass {
     {
         // prologue: x0 row 0 (+ coarse rows -1, 0), then the groups steps
         // -3..-1 would have issued
+        if constexpr (CL > 1) {                          // zeroed slots, then the mbarriers
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                mbar_init(mb_tot, 1);
+                mbar_init(mb_hr, 1);
+                mbar_init(mb_res, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            }
+        }
         sync_pair();                                     // zeroed slots before any copy lands
-                                                         // (or any store of the other strip)
+                                                         // (or any message of the other strip)
         if constexpr (!(DOWN && ZS)) {
             stage_row<true, LX0>(x0sm, Xg, 0);
             if constexpr (!DOWN) {
@@ -807,6 +890,9 @@ struct RegPass {
         for (; t < nsteps; t += 2) {
             step<true, 0>(t);
             if (t + 1 < nsteps) step<true, 1>(t + 1);
+        }
+        if constexpr (CL > 1) {                          // the last halo message lands before exit
+            if (!lstrip && warp == NW - 1 && lane == 31) mbar_wait(mb_hr, (nsteps - 1) & 1);
         }
         cp_async_wait<0>();
     }
@@ -927,11 +1013,15 @@ cudaError_t mg2d_reg_launch(const MgStreamArgs &a, bool down, int64_t rows, cuda
             return launch_reg_n<4, 256, 1>(a, down, rows, st);
         return launch_reg_n<8, 128, 2>(a, down, rows, st);
     case 2047:
-        // two 128-thread strips per row on a CTA pair (two rows per SM);
-        // HWG_REG_CLUSTER=0: one 256-thread CTA per row (A/B)
+        // HWG_REG_CLUSTER=1 (A/B, bit-identical): the row as two 128-thread
+        // strips on a CTA pair (RegPass CL = 2).  Measured slower
+        // (profiles/r02/mg_cluster_strips.txt): a row still needs 256 x 255
+        // registers, so an SM pair holds two rows either way, and the
+        // per-step messages cost what the 8-warp barriers did
         if (const char *ev = getenv("HWG_REG_CLUSTER"))
-            if (ev[0] == '0') return launch_reg_n<8, 256, 1>(a, down, rows, st);
-        return launch_reg_n<8, 128, 2, 2>(a, down, rows, st);
+            if (ev[0] == '1') return launch_reg_n<8, 128, 2, 2>(a, down, rows, st);
+        if (wide & (1 << 11)) return launch_reg_n<4, 512, 1>(a, down, rows, st);
+        return launch_reg_n<8, 256, 1>(a, down, rows, st);
     default: return cudaErrorNotSupported;
     }
 }

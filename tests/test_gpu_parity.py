@@ -281,6 +281,42 @@ def test_mg_rows_fused_inner_product(K):
     assert float(((p1 - p2).abs() / scale).max()) <= 1e-14
 
 
+@pytest.mark.parametrize("domain", ["square", "L"])
+def test_cluster_strips_bit_identical(domain, monkeypatch):
+    """The n = 2047 level pass as two column strips on a thread-block cluster
+    (HWG_REG_CLUSTER=1: carry windows and halos as st.async messages between
+    the CTA pair) reproduces the one-CTA kernel bit for bit, fused inner
+    product included."""
+    from paper_2009_08875_b200.device import GpuContext
+
+    kw = {"domain": "L", "D": 0.25 * np.eye(2)} if domain == "L" else {}
+    ctx = GpuContext(2, 2, 11, **kw)
+    rows, nx = 5, ctx.n_x
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    B = torch.randn((rows, nx), dtype=torch.float64, device="cuda", generator=gen)
+    Y = torch.randn((rows, nx), dtype=torch.float64, device="cuda", generator=gen)
+    if domain == "L":                      # the row kernels work on the embedded grid layout
+        Bg, Yg = (torch.zeros((rows, ctx.n_grid), dtype=torch.float64, device="cuda") for _ in range(2))
+        ctx.grid_scatter(B, Bg)
+        ctx.grid_scatter(Y, Yg)
+        B, Y = Bg, Yg
+    ops = torch.tensor([0, 1, 2, 3, 1], dtype=torch.int32, device="cuda")
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HWG_REG_CLUSTER", mode)
+        X = torch.empty_like(B)
+        Xd = torch.empty_like(B)
+        p = torch.empty(rows, dtype=torch.float64, device="cuda")
+        ctx.mg_rows_dev(ops, B, X)
+        ctx.mg_rows_dev_dot(ops, B, Xd, Y, p)
+        torch.cuda.synchronize()
+        out[mode] = (X, Xd, p)
+    assert torch.equal(out["0"][0], out["1"][0])
+    assert torch.equal(out["0"][1], out["1"][1])
+    scale = (Y.abs() * out["0"][0].abs()).sum(dim=1)
+    assert float(((out["0"][2] - out["1"][2]).abs() / scale).max()) <= 1e-14
+
+
 def test_pcg_residual_recomputation_matches_oracle():
     """recompute_every = 4 (solver.py:227-229: r = f - S w every 4th step)
     exercises the un-deferred w update path; iterations and u as the oracle."""
