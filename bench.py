@@ -429,7 +429,11 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "launches": dn, "bytes_per_launch": dbytes / max(dn, 1),
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         **({"note": "mg1d is FP64-issue/latency-bound, not HBM-bound: ncu has the FP64 "
+                                     "pipe 45 % busy and DRAM 14 % (profiles/r02/ncu_mg1d_rrp.txt); its "
+                                     "16 B/point of traffic is the compulsory minimum"}
+                            if dname == "mg1d" else {})},
             "roofline_iteration": {"bytes_per_iteration": impl_b, "s_per_iteration": it_s,
                                    "achieved_GBs": impl_b / it_s / 1e9, "peak": peak,
                                    "frac": impl_b / it_s / 1e9 / peak,
