@@ -79,7 +79,18 @@ HW_DEV void store_b(double *s, int t, const double (&v)[RL<L>::C])
 }
 
 // carry into lane t from the zero-carry chunk ends S of the lanes before it
-// (forward: t-1, t-2, ...; backward: t+1, t+2, ...), gamma = beta^C
+// (forward: t-1, t-2, ...; backward: t+1, t+2, ...), gamma = beta^C, truncated
+// after W = 64 / C chunks: sum_{k=1..W} gamma^(k-1) S(t-k).  A 64-bit shuffle
+// costs ~27 cycles and sits on the sweep's critical path (a DFMA 8), so for
+// small chunks (C <= kPfMaxC, W >= 8: the scan is most of the sweep) the window
+// is summed with few DEPENDENT shuffles: log2(W/4) doubling rounds build block
+// sums of B = W/4 chunks, then the four blocks are fetched with independent
+// shuffles and combined by Horner.  Larger chunks keep the plain doubling scan
+// (fewer live registers where the level's iterate is large).
+#ifndef RR_PF_MAXC
+#define RR_PF_MAXC 8
+#endif
+constexpr int kPfMaxC = RR_PF_MAXC;
 template <int C, bool FWD>
 HW_DEV double lane_carry(double S, double gam, int lane)
 {
@@ -92,6 +103,19 @@ HW_DEV double lane_carry(double S, double gam, int lane)
         const double s1 = sh(S, 1), s2 = sh(S, 2);
         const double a = has(1) ? s1 : 0.0, b = has(2) ? s2 : 0.0;
         return fma(gam, b, a);
+    } else if constexpr (C <= kPfMaxC && W >= 4 && W <= 32) {
+        constexpr int B = W / 4;
+        double T = S, g = gam;
+#pragma unroll
+        for (int o = 1; o < B; o <<= 1) {              // T(t) = sum_{k<2o} gamma^k S(t-k)
+            const double v = sh(T, o);
+            T = fma(g, has(o) ? v : 0.0, T);
+            g *= g;
+        }
+        const double v0 = sh(T, 1), v1 = sh(T, 1 + B), v2 = sh(T, 1 + 2 * B), v3 = sh(T, 1 + 3 * B);
+        const double a0 = has(1) ? v0 : 0.0, a1 = has(1 + B) ? v1 : 0.0;
+        const double a2 = has(1 + 2 * B) ? v2 : 0.0, a3 = has(1 + 3 * B) ? v3 : 0.0;
+        return fma(g, fma(g, fma(g, a3, a2), a1), a0);   // g = gamma^B
     } else {
         double T = S, g = gam;
 #pragma unroll
