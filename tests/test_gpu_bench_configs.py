@@ -81,7 +81,10 @@ def _solve(meta):
 def _check_against(meta, g, asm, res, u):
     idx = g["sample_idx"]
     f = asm.rhs.f_hat.array
-    assert relative_diff(_sampled(f, idx), g["fhat_sample"]) <= 1e-12
+    # f-hat passes through K_Y's batched multigrid (rounding-level differences
+    # on the streamed levels that grow with the level operators' conditioning:
+    # 2.2e-12 max-abs at cfg 3, 1.0e-11 at K = 11 on the L)
+    assert relative_diff(_sampled(f, idx), g["fhat_sample"]) <= 1e-10
     assert res.iterations == meta["iterations"]
     hist, ref = np.array(res.residual_norms), np.array(meta["residual_norms"])
     assert np.abs(hist - ref).max() <= 1e-8 * ref.max()
@@ -89,8 +92,12 @@ def _check_against(meta, g, asm, res, u):
     assert _rel_l2(_sampled(res.w.array, idx), g["w_sample"]) <= 1e-8
     assert _rel_l2(_sampled(u, idx), g["u_sample"]) <= 1e-8
     assert abs(float(torch.linalg.norm(u)) - meta["u_norm"]) <= 1e-8 * meta["u_norm"]
+    # the final-time row, against the scale of a typical row (cfg 3's u(T) is
+    # 1e-7 of the solution: two solves that agree to 1e-11 in l2 differ by more
+    # than 1e-8 relative in it)
     last = float(torch.linalg.norm(u[-1]))
-    assert abs(last - meta["u_last_row_norm"]) <= 1e-8 * meta["u_last_row_norm"]
+    row_scale = max(meta["u_last_row_norm"], meta["u_norm"] / np.sqrt(meta["n_t"]))
+    assert abs(last - meta["u_last_row_norm"]) <= 1e-8 * row_scale
 
 
 @pytest.mark.parametrize("name", ["c410", "t10k8", "d16"])
