@@ -162,9 +162,23 @@ __global__ void __launch_bounds__(kWavBS) wav_syn_pairs2(const double *__restric
         }
         return;
     }
-    auto Cr = [&](int q) { return C[(int64_t)q * nx + i]; };
-    auto D1 = [&](int k) { return Dm[(int64_t)k * nx + i]; };
-    auto D2 = [&](int k) { return Dm2[(int64_t)k * nx + i]; };
+    // every row the tile reads, loaded up front (37 independent loads in flight
+    // per thread; read one by one inside the dependent recurrence below, the
+    // kernel ran at 4.6 TB/s): c[u] = C[q0 + u], d1[u] = D_j[q0 - 1 + u],
+    // d2[v] = D_{j+1}[f0 - 1 + v]; rows that do not exist are never used
+    double c[kWavQP2 + 1], d1[kWavQP2 + 2], d2[2 * kWavQP2 + 2];
+#pragma unroll
+    for (int u = 0; u <= kWavQP2; ++u) c[u] = q0 + u <= nw ? C[(int64_t)(q0 + u) * nx + i] : 0.0;
+#pragma unroll
+    for (int u = 0; u <= kWavQP2 + 1; ++u) {
+        const int k = q0 - 1 + u;
+        d1[u] = (k >= 0 && k < nw) ? Dm[(int64_t)k * nx + i] : 0.0;
+    }
+#pragma unroll
+    for (int v = 0; v <= 2 * kWavQP2 + 1; ++v) {
+        const int k = f0 - 1 + v;
+        d2[v] = (k >= 0 && k < nw2) ? Dm2[(int64_t)k * nx + i] : 0.0;
+    }
     // F[2q] and F[2q+1] of stage j (wav_syn_pairs' arithmetic)
     auto Feven = [&](int q, double cq, double dm, double dq) {
         double acc = cq;
@@ -178,12 +192,11 @@ __global__ void __launch_bounds__(kWavBS) wav_syn_pairs2(const double *__restric
         return add_rn(od, mul_rn(s, dq));
     };
     // G[2f], G[2f+1] of stage j+1 from F[f], F[f+1] (F[f+1] unused if f == nw2)
-    double gdm = f0 >= 1 ? D2(f0 - 1) : 0.0;              // d2[f-1]
-    auto emit = [&](int f, double Ff, double Fn) {
+    double gdm = d2[0];                                   // d2[f-1]
+    auto emit = [&](int f, double dq, double Ff, double Fn) {   // dq = D_{j+1}[f]
         double acc = Ff;
         if (f >= 1) acc = add_rn(acc, mul_rn(qb(s2, f - 1, nw2), gdm));
         if (f < nw2) {
-            const double dq = D2(f);
             acc = add_rn(acc, mul_rn(qa(s2, f), dq));
             double od = mul_rn(0.5, Ff);
             od = add_rn(od, mul_rn(0.5, Fn));
@@ -193,33 +206,33 @@ __global__ void __launch_bounds__(kWavBS) wav_syn_pairs2(const double *__restric
         }
         Y[(int64_t)(2 * f) * nx + i] = acc;
     };
-    double cq = Cr(q0);
-    double dm = q0 >= 1 ? D1(q0 - 1) : 0.0;
+    double cq = c[0];
+    double dm = d1[0];
     double Fprev = 0.0;                                   // F[f-1], pending emission
     bool pending = false;
 #pragma unroll
     for (int u = 0; u < kWavQP2; ++u) {
         const int q = q0 + u;
         if (q >= q1) break;
-        const double dq = q < nw ? D1(q) : 0.0;
+        const double dq = d1[u + 1];                      // D_j[q] (0 past the last wavelet)
         const double fe = Feven(q, cq, dm, dq);           // F[2q]
-        if (pending) emit(2 * q - 1, Fprev, fe);
+        if (pending) emit(2 * q - 1, d2[2 * u], Fprev, fe);
         if (q < nw) {
-            const double cn = Cr(q + 1);
+            const double cn = c[u + 1];
             const double fo = Fodd(cq, cn, dq);           // F[2q+1]
-            emit(2 * q, fe, fo);
+            emit(2 * q, d2[2 * u + 1], fe, fo);
             Fprev = fo;
             pending = true;
             cq = cn;
             dm = dq;
         } else {
-            emit(2 * q, fe, 0.0);                         // F[2 nw] = the last fine node
+            emit(2 * q, d2[2 * u + 1], fe, 0.0);          // F[2 nw] = the last fine node
             pending = false;
         }
     }
-    if (pending) {                                        // F[2 q1 - 1] needs F[2 q1]
-        const double dq = q1 < nw ? D1(q1) : 0.0;
-        emit(2 * q1 - 1, Fprev, Feven(q1, cq, dm, dq));
+    if (pending) {                                        // F[2 q1 - 1] needs F[2 q1]; pending
+        const double dq = d1[kWavQP2 + 1];                // implies q1 = q0 + kWavQP2 <= nw
+        emit(2 * q1 - 1, d2[2 * kWavQP2], Fprev, Feven(q1, cq, dm, dq));
     }
 }
 
@@ -280,20 +293,20 @@ __global__ void __launch_bounds__(kWavBS) wav_ana_pairs2(const double *__restric
     const int fb = fs < 0 ? 0 : fs;
     const int fe = min(2 * r1, nw2);
     double F[NFV];
-    double xa = fb >= 1 ? Xr(2 * fb - 1) : 0.0, xb = Xr(2 * fb);
+    // x rows 2 fs - 1 .. 2 (fs + NFV - 1) + 2, all loaded up front (independent
+    // loads in flight instead of two per step of the loop below)
+    double xr[2 * NFV + 2];
+#pragma unroll
+    for (int v = 0; v < 2 * NFV + 2; ++v) {
+        const int k = 2 * fs - 1 + v;
+        xr[v] = (k >= (fb >= 1 ? 2 * fb - 1 : 0) && k < nf2 && k <= 2 * fe + 2) ? Xr(k) : 0.0;
+    }
 #pragma unroll
     for (int t = 0; t < NFV; ++t) {
         const int f = fs + t;
         F[t] = 0.0;
         if (f < fb || f > fe) continue;
-        double xc = 0.0, xd = 0.0;
-        if (2 * f + 1 < nf2) {
-            xc = Xr(2 * f + 1);
-            xd = Xr(2 * f + 2);
-        }
-        F[t] = stage2(f, xa, xb, xc, xd, f >= f0 && f < f1);
-        xa = xc;
-        xb = xd;
+        F[t] = stage2(f, xr[2 * t], xr[2 * t + 1], xr[2 * t + 2], xr[2 * t + 3], f >= f0 && f < f1);
     }
     // stage j (wav_ana_pairs on F): C[r], d_j[r]
 #pragma unroll
