@@ -78,8 +78,11 @@ def impl_bytes_per_iteration(d, J, K, cycles=2):  # grid layout (the L moves its
     n_x = size[K]
     N = n_t * n_x
     # W: stage j reads 2^(j-1)+1 coarse + 2^(j-1) wavelet rows, writes 2^j + 1;
-    # W^T: stage j reads 2^j + 1 rows, writes 2^(j-1)+1 + 2^(j-1)
-    wav = sum(2 * (2 ** j + 1) for j in range(1, J + 1)) * n_x
+    # W^T: stage j reads 2^j + 1 rows, writes 2^(j-1)+1 + 2^(j-1).  The top two
+    # stages run as one pass (hw_wavelet.cu: the stage J-1 prefix stays in
+    # registers), so stage J-1's 2 (2^(J-1) + 1) rows are not moved
+    fused_top = J >= 2
+    wav = sum(2 * (2 ** j + 1) for j in range(1, J + 1) if not (fused_top and j == J - 1)) * n_x
 
     def mg_words_per_row():
         if d == 1:
