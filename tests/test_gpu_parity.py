@@ -281,6 +281,31 @@ def test_mg_rows_fused_inner_product(K):
     assert float(((p1 - p2).abs() / scale).max()) <= 1e-14
 
 
+@pytest.mark.parametrize("K", [7, 8, 9, 10])
+def test_mg1d_register_hierarchy_matches_mg1d_reg(K, monkeypatch):
+    """mg1d_rrp (persistent, every streamed level in registers, dense level-6
+    operator in shared memory) against mg1d_reg (exact scans, pinned to the
+    reference by mg1d10 / d2) for every K it serves, on batches that do not
+    fill a tile, mixed operators within a tile and a single operator."""
+    from paper_2009_08875_b200.device import GpuContext
+
+    J = 6
+    monkeypatch.setenv("HWG_MG1D", "1")
+    ref = GpuContext(1, J, K)
+    monkeypatch.delenv("HWG_MG1D")
+    ctx = GpuContext(1, J, K)
+    gen = torch.Generator(device="cuda").manual_seed(K)
+    for rows in (1, 13, 2 * ctx.n_t):
+        B = torch.randn((rows, ctx.n_x), dtype=torch.float64, device="cuda", generator=gen)
+        for ops in (torch.randint(0, J + 2, (rows,), dtype=torch.int32, device="cuda", generator=gen),
+                    torch.full((rows,), J + 1, dtype=torch.int32, device="cuda")):
+            X, Xr = torch.empty_like(B), torch.empty_like(B)
+            ctx.mg_rows_dev(ops, B, X)
+            ref.mg_rows_dev(ops, B, Xr)
+            torch.cuda.synchronize()
+            assert float((X - Xr).abs().max() / Xr.abs().max()) <= 1e-11, (rows, K)
+
+
 @pytest.mark.parametrize("domain", ["square", "L"])
 def test_cluster_strips_bit_identical(domain, monkeypatch):
     """The n = 2047 level pass as two column strips on a thread-block cluster
