@@ -480,6 +480,139 @@ __device__ __forceinline__ SPt strip_pt(int i0, int r, int c, const Grid &g)
     return p;
 }
 
+// ---- bside_stack: bside_fused with R vertically stacked points per thread --
+// A thread owns column j of R consecutive grid rows, so the R 7-point
+// stencils of one temporal row share their loads: (R + 2) x 3 values instead
+// of 7 R (4.5 instead of 7 per point at R = 4).  The loads stay coalesced
+// along j and the arithmetic per point is stencil2's (CSR column order,
+// absent couplings skipped): bit-identical.  bside_fused is bound by L1
+// wavefronts (rows of odd length: a warp's 256 bytes span three 128-byte
+// lines per load) -- fewer loads per point is the lever.  2D only.
+template <bool DIAG>
+__device__ __forceinline__ double stencil_vals(const double (&a)[3], const double (&b)[3],
+                                               const double (&c)[3], int i, int j, int m,
+                                               bool interior, const Stencil &s)
+{
+    // a, b, c: grid rows i-1, i, i+1 at columns j-1, j, j+1
+    if (interior) {
+        double acc;
+        if (DIAG) {
+            acc = mul_rn(s.cd, a[0]);
+            acc = add_rn(acc, mul_rn(s.cx, a[1]));
+        } else {
+            acc = mul_rn(s.cx, a[1]);
+        }
+        acc = add_rn(acc, mul_rn(s.cy, b[0]));
+        acc = add_rn(acc, mul_rn(s.c0, b[1]));
+        acc = add_rn(acc, mul_rn(s.cy, b[2]));
+        acc = add_rn(acc, mul_rn(s.cx, c[1]));
+        if (DIAG) acc = add_rn(acc, mul_rn(s.cd, c[2]));
+        return acc;
+    }
+    double acc = 0.0;
+    bool first = true;
+    auto add = [&](double v) { acc = first ? v : add_rn(acc, v); first = false; };
+    if (DIAG && i > 0 && j > 0) add(mul_rn(s.cd, a[0]));
+    if (i > 0) add(mul_rn(s.cx, a[1]));
+    if (j > 0) add(mul_rn(s.cy, b[0]));
+    add(mul_rn(s.c0, b[1]));
+    if (j < m - 1) add(mul_rn(s.cy, b[2]));
+    if (i < m - 1) add(mul_rn(s.cx, c[1]));
+    if (DIAG && i < m - 1 && j < m - 1) add(mul_rn(s.cd, c[2]));
+    return acc;
+}
+
+template <bool DM, bool DA, int R>
+__global__ void __launch_bounds__(TX * TY) bside_stack(const double *__restrict__ U, int64_t u0,
+                                                       double *__restrict__ T1,
+                                                       double *__restrict__ T2,
+                                                       double *__restrict__ E0, Grid g,
+                                                       Stencil M, Stencil A, Tri4 tri,
+                                                       int64_t r0, int64_t nr, int64_t nt,
+                                                       int chunk)
+{
+    const int m = g.m;
+    const int j = blockIdx.x * TX + threadIdx.x;
+    const int ib = (blockIdx.y * TY + threadIdx.y) * R;
+    if (j >= m || ib >= m) return;
+    const int64_t k0 = (int64_t)ib * m + j;              // point (ib, j)
+    const double *Uk = U + k0;
+    bool in[R], msk[R], ok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const Pt p{ib + r, j, ib + r < m};
+        ok[r] = p.ok;
+        in[r] = interior_of(p, g);
+        msk[r] = masked_pt(p, g);
+    }
+    // (M_x U, A_x U) of temporal row c at the R points
+    auto st = [&](int64_t c, double (&mv)[R], double (&av)[R]) {
+        const double *x = Uk + (c - u0) * g.nx;
+        double v[R + 2][3];
+#pragma unroll
+        for (int rr = 0; rr < R + 2; ++rr) {
+            const int i = ib - 1 + rr;
+            const bool rowok = i >= 0 && i < m;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const int jj = j - 1 + cc;
+                // the corners (ib-1, j+1) and (ib+R, j-1) couple to no owned point;
+                // (ib-1, j-1) and (ib+R, j+1) only through the diagonal
+                const bool need = rr == 0 ? (cc == 1 || (cc == 0 && (DM || DA)))
+                                          : (rr == R + 1 ? (cc == 1 || (cc == 2 && (DM || DA))) : true);
+                v[rr][cc] = (need && rowok && jj >= 0 && jj < m)
+                                ? __ldg(x + (int64_t)(rr - 1) * m + (cc - 1))
+                                : 0.0;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!ok[r] || msk[r]) {                       // zero rows -> zero bands
+                mv[r] = av[r] = 0.0;
+                continue;
+            }
+            mv[r] = stencil_vals<DM>(v[r], v[r + 1], v[r + 2], ib + r, j, m, in[r], M);
+            av[r] = stencil_vals<DA>(v[r], v[r + 1], v[r + 2], ib + r, j, m, in[r], A);
+        }
+    };
+    for (int64_t c0 = r0 + (int64_t)blockIdx.z * chunk; c0 < r0 + nr;
+         c0 += (int64_t)gridDim.z * chunk) {
+        const int64_t c1 = c0 + chunk < r0 + nr ? c0 + chunk : r0 + nr;
+        double mm[R], am[R], m0[R], a0[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) mm[r] = am[r] = 0.0;  // row c-1
+        if (c0 > 0) st(c0 - 1, mm, am);
+        st(c0, m0, a0);
+        if (c0 == 0 && E0) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (ok[r]) E0[k0 + (int64_t)r * m] = m0[r];
+        }
+        for (int64_t c = c0; c < c1; ++c) {
+            if (c + kBsidePf < nt && c + kBsidePf < c1 + 1) {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (ok[r])
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(Uk + (c + kBsidePf - u0) * g.nx +
+                                                                      (int64_t)r * m));
+            }
+            double mp[R], ap[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) mp[r] = ap[r] = 0.0;  // row c+1
+            if (c + 1 < nt) st(c + 1, mp, ap);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!ok[r]) continue;
+                const int64_t o = (c - r0) * g.nx + k0 + (int64_t)r * m;
+                T1[o] = add_rn(band3(tri.At, c, mm[r], m0[r], mp[r]), band3(tri.LT, c, am[r], a0[r], ap[r]));
+                T2[o] = add_rn(band3(tri.Mt, c, am[r], a0[r], ap[r]), band3(tri.L, c, mm[r], m0[r], mp[r]));
+                mm[r] = m0[r]; am[r] = a0[r];
+                m0[r] = mp[r]; a0[r] = ap[r];
+            }
+        }
+    }
+}
+
 // bside_fused on TMA-staged strips: the same sliding window over temporal
 // rows (FY x CJ points per consumer thread), stencils from shared memory
 template <bool DM, bool DA, int FY, int CJ>
@@ -900,6 +1033,24 @@ cudaError_t launch_bside_fused(const double *U, int64_t u0, int64_t nu, double *
         case 2: return launch_bside_strip<2, 2>(U, u0, nu, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk, st);
         default: return launch_bside_strip<1, 4>(U, u0, nu, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk, st);
         }
+    }
+    static const bool stack = [] {                       // HWG_BSIDE_STACK=0: one point per thread (A/B)
+        const char *ev = getenv("HWG_BSIDE_STACK");
+        return !(ev && ev[0] == '0');
+    }();
+    if (g.dim == 2 && stack) {
+        constexpr int R = 4;
+        dim3 gs = grid;
+        gs.y = (unsigned)((g.m + TY * R - 1) / (TY * R));
+        if (dm && da)
+            bside_stack<true, true, R><<<gs, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+        else if (dm)
+            bside_stack<true, false, R><<<gs, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+        else if (da)
+            bside_stack<false, true, R><<<gs, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+        else
+            bside_stack<false, false, R><<<gs, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
+        return cudaGetLastError();
     }
     if (dm && da)
         bside_fused<true, true><<<grid, block, 0, st>>>(U, u0, T1, T2, E0, g, M, A, tri, r0, nr, nt, chunk);
