@@ -29,7 +29,3 @@ timed(lambda: a.sum(), 8 * n, "read only (sum)")
 timed(lambda: b.fill_(1.0), 8 * n, "write only (fill)")
 timed(lambda: b.copy_(a), 16 * n, "1 read : 1 write (copy)")
 timed(lambda: torch.add(a, b, out=c), 24 * n, "2 reads : 1 write (add)")
-# 1 read : 2 writes, one kernel: torch.var_mean / sincos have no elementwise pair op on
-# fp64 tensors without extra passes; two outputs through a fused foreach op:
-x = [a]
-timed(lambda: (torch._foreach_mul(x, 2.0), None), 16 * n, "foreach mul (1 read : 1 write, alloc)")
