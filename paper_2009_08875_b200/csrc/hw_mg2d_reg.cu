@@ -46,6 +46,11 @@
 //    (DOWN: the masked part of a row is a suffix; UP, point-reversed, a
 //    prefix).  Masked residuals are zero before restriction; prolongation
 //    needs nothing (masked fine points interpolate masked coarse zeros).
+//  * Thread shapes: P = 8 points per thread by default; contexts with a short
+//    time axis run levels 7-9 with twice the threads (mg2d_reg_launch).
+//  * CL = 2 (opt-in, n = 2047): the grid row as two column strips on a
+//    thread-block cluster; the strips exchange carry windows and halos as
+//    st.async messages that complete the receiver's mbarrier (RegPass).
 #include "hw_common.cuh"
 #include "hw_internal.cuh"
 
